@@ -1,0 +1,20 @@
+"""B200-native mixed-precision Sylvester / Lyapunov solver (arXiv 2503.03456).
+
+Drop-in for the hot path of the reference package ``mpsylv``: the solver
+entry points ``mp_orth`` / ``mp_inv`` / ``solve_pert_sylv_tri_stat`` with the
+reference's ``SylvesterProblem`` / ``RefinementConfig`` / ``SolveReport`` and
+exception types, backed by hand-written sm_100a CUDA kernels behind the C ABI
+in ``include/mpsylv_b200.h``.  ``solve`` is the torch-native entry.
+"""
+
+from .costmodel import FlopCount, flops
+from .errors import (DeviceError, DimensionError, FormatOverflowError, IterationLimitError, MpsylvError,
+                     NotHermitianError, NumericBreakdownError, PrecisionOverflowWarning, RankDeficiencyError,
+                     SingularEquationError, SingularMatrixError, UnsupportedPrecisionError)
+from .precision import (B24, BFLOAT16, BINARY16, BINARY32, BINARY64, FORMATS, TF32, FlopCounter, FpFormat,
+                        PrecisionContext, format_from_name, parse_format)
+from .refinement import RefinementConfig, SolveReport, mp_inv, mp_orth, solve, solve_pert_sylv_tri_stat
+from .sylvester import SylvesterProblem, residual, solve_sylv_tri
+from .linalg import QrFactors, SchurFactors, gemm, mgs_qr, schur
+
+__version__ = "0.1.0"

@@ -1,0 +1,200 @@
+// common.cuh -- scalar types, complex arithmetic, launch helpers.
+//
+// Layout convention of the whole library: column-major matrices with an
+// explicit leading dimension (element (i,j) of M at M[i + j*ld]).
+// Scalar codes (the C-ABI `dtype`): 0 = float (s), 1 = double (d),
+// 2 = complex<float> (c), 3 = complex<double> (z).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <math.h>
+
+namespace msy {
+
+template <class R>
+struct cplx {
+  R x, y;
+  __host__ __device__ cplx() {}
+  __host__ __device__ constexpr cplx(R re, R im = R(0)) : x(re), y(im) {}
+};
+typedef cplx<float> cfloat;
+typedef cplx<double> cdouble;
+
+template <class R> __host__ __device__ __forceinline__ cplx<R> operator+(cplx<R> a, cplx<R> b) { return cplx<R>(a.x + b.x, a.y + b.y); }
+template <class R> __host__ __device__ __forceinline__ cplx<R> operator-(cplx<R> a, cplx<R> b) { return cplx<R>(a.x - b.x, a.y - b.y); }
+template <class R> __host__ __device__ __forceinline__ cplx<R> operator-(cplx<R> a) { return cplx<R>(-a.x, -a.y); }
+template <class R> __host__ __device__ __forceinline__ cplx<R> operator*(cplx<R> a, cplx<R> b) {
+  return cplx<R>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <class R> __host__ __device__ __forceinline__ cplx<R> operator*(R a, cplx<R> b) { return cplx<R>(a * b.x, a * b.y); }
+template <class R> __host__ __device__ __forceinline__ cplx<R> operator*(cplx<R> b, R a) { return cplx<R>(a * b.x, a * b.y); }
+template <class R> __host__ __device__ __forceinline__ cplx<R>& operator+=(cplx<R>& a, cplx<R> b) { a.x += b.x; a.y += b.y; return a; }
+template <class R> __host__ __device__ __forceinline__ cplx<R>& operator-=(cplx<R>& a, cplx<R> b) { a.x -= b.x; a.y -= b.y; return a; }
+template <class R> __host__ __device__ __forceinline__ bool operator==(cplx<R> a, cplx<R> b) { return a.x == b.x && a.y == b.y; }
+template <class R> __host__ __device__ __forceinline__ bool operator!=(cplx<R> a, cplx<R> b) { return !(a == b); }
+
+// Smith division (the reference's own complex division, precision.py:462-479)
+template <class R>
+__host__ __device__ __forceinline__ cplx<R> operator/(cplx<R> a, cplx<R> b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    R t = b.y / b.x, d = b.x + b.y * t;
+    return cplx<R>((a.x + a.y * t) / d, (a.y - a.x * t) / d);
+  }
+  R t = b.x / b.y, d = b.y + b.x * t;
+  return cplx<R>((a.y + a.x * t) / d, -(a.x - a.y * t) / d);
+}
+template <class R> __host__ __device__ __forceinline__ cplx<R> operator/(cplx<R> a, R b) { return cplx<R>(a.x / b, a.y / b); }
+
+// ---- scalar traits -------------------------------------------------------
+template <class S> struct tr;
+template <> struct tr<float> {
+  typedef float R; static constexpr bool cx = false; static constexpr int code = 0;
+  __host__ __device__ static constexpr float u() { return 5.9604644775390625e-08f; }  // 2^-24
+};
+template <> struct tr<double> {
+  typedef double R; static constexpr bool cx = false; static constexpr int code = 1;
+  __host__ __device__ static constexpr double u() { return 1.1102230246251565e-16; }  // 2^-53
+};
+template <> struct tr<cfloat> {
+  typedef float R; static constexpr bool cx = true; static constexpr int code = 2;
+  __host__ __device__ static constexpr float u() { return 5.9604644775390625e-08f; }
+};
+template <> struct tr<cdouble> {
+  typedef double R; static constexpr bool cx = true; static constexpr int code = 3;
+  __host__ __device__ static constexpr double u() { return 1.1102230246251565e-16; }
+};
+
+template <class S> struct lowp;  // the matching low/high precision
+template <> struct lowp<double> { typedef float T; };
+template <> struct lowp<cdouble> { typedef cfloat T; };
+template <class S> struct highp;
+template <> struct highp<float> { typedef double T; };
+template <> struct highp<cfloat> { typedef cdouble T; };
+
+__host__ __device__ __forceinline__ float re(float a) { return a; }
+__host__ __device__ __forceinline__ double re(double a) { return a; }
+template <class R> __host__ __device__ __forceinline__ R re(cplx<R> a) { return a.x; }
+__host__ __device__ __forceinline__ float im(float) { return 0.f; }
+__host__ __device__ __forceinline__ double im(double) { return 0.0; }
+template <class R> __host__ __device__ __forceinline__ R im(cplx<R> a) { return a.y; }
+__host__ __device__ __forceinline__ float conj(float a) { return a; }
+__host__ __device__ __forceinline__ double conj(double a) { return a; }
+template <class R> __host__ __device__ __forceinline__ cplx<R> conj(cplx<R> a) { return cplx<R>(a.x, -a.y); }
+__host__ __device__ __forceinline__ float abs2(float a) { return a * a; }
+__host__ __device__ __forceinline__ double abs2(double a) { return a * a; }
+template <class R> __host__ __device__ __forceinline__ R abs2(cplx<R> a) { return a.x * a.x + a.y * a.y; }
+__host__ __device__ __forceinline__ float absv(float a) { return fabsf(a); }
+__host__ __device__ __forceinline__ double absv(double a) { return fabs(a); }
+template <class R> __host__ __device__ __forceinline__ R absv(cplx<R> a) { return hypot(a.x, a.y); }
+// |re| + |im| (cheap magnitude used for deflation / scaling decisions)
+__host__ __device__ __forceinline__ float abs1(float a) { return fabsf(a); }
+__host__ __device__ __forceinline__ double abs1(double a) { return fabs(a); }
+template <class R> __host__ __device__ __forceinline__ R abs1(cplx<R> a) { return fabs(a.x) + fabs(a.y); }
+__host__ __device__ __forceinline__ bool isfin(float a) { return isfinite(a); }
+__host__ __device__ __forceinline__ bool isfin(double a) { return isfinite(a); }
+template <class R> __host__ __device__ __forceinline__ bool isfin(cplx<R> a) { return isfinite(a.x) && isfinite(a.y); }
+__host__ __device__ __forceinline__ bool iszero(float a) { return a == 0.f; }
+__host__ __device__ __forceinline__ bool iszero(double a) { return a == 0.0; }
+template <class R> __host__ __device__ __forceinline__ bool iszero(cplx<R> a) { return a.x == R(0) && a.y == R(0); }
+
+template <class S> __host__ __device__ __forceinline__ S mk(typename tr<S>::R r, typename tr<S>::R i = 0);
+template <> __host__ __device__ __forceinline__ float mk<float>(float r, float) { return r; }
+template <> __host__ __device__ __forceinline__ double mk<double>(double r, double) { return r; }
+template <> __host__ __device__ __forceinline__ cfloat mk<cfloat>(float r, float i) { return cfloat(r, i); }
+template <> __host__ __device__ __forceinline__ cdouble mk<cdouble>(double r, double i) { return cdouble(r, i); }
+
+// a*b + c  (FMA for real, 4 FMAs for complex)
+__device__ __forceinline__ float fmac(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmac(double a, double b, double c) { return fma(a, b, c); }
+template <class R> __device__ __forceinline__ cplx<R> fmac(cplx<R> a, cplx<R> b, cplx<R> c) {
+  return cplx<R>(fma(-a.y, b.y, fma(a.x, b.x, c.x)), fma(a.y, b.x, fma(a.x, b.y, c.y)));
+}
+// conj(a)*b + c
+__device__ __forceinline__ float fmacc(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmacc(double a, double b, double c) { return fma(a, b, c); }
+template <class R> __device__ __forceinline__ cplx<R> fmacc(cplx<R> a, cplx<R> b, cplx<R> c) {
+  return cplx<R>(fma(a.y, b.y, fma(a.x, b.x, c.x)), fma(-a.y, b.x, fma(a.x, b.y, c.y)));
+}
+
+// conversions between precisions (exact widening, rounding narrowing)
+__host__ __device__ __forceinline__ float cvt(float a, float*) { return a; }
+__host__ __device__ __forceinline__ double cvt(float a, double*) { return (double)a; }
+__host__ __device__ __forceinline__ float cvt(double a, float*) { return (float)a; }
+__host__ __device__ __forceinline__ double cvt(double a, double*) { return a; }
+template <class R1, class R2> __host__ __device__ __forceinline__ cplx<R2> cvt(cplx<R1> a, cplx<R2>*) { return cplx<R2>((R2)a.x, (R2)a.y); }
+template <class D, class Sx> __host__ __device__ __forceinline__ D conv(Sx a) { return cvt(a, (D*)0); }
+
+// shuffles for complex / double
+template <class S> __device__ __forceinline__ S shfl(S v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+template <> __device__ __forceinline__ cfloat shfl<cfloat>(cfloat v, int src) {
+  return cfloat(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+template <> __device__ __forceinline__ cdouble shfl<cdouble>(cdouble v, int src) {
+  return cdouble(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+template <class R> __device__ __forceinline__ R warp_sum(R v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <class R> __device__ __forceinline__ cplx<R> warp_sum(cplx<R> v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// deterministic block reduction (fixed order); `buf` needs blockDim/32 entries
+template <class V>
+__device__ __forceinline__ V block_sum(V v, V* buf) {
+  v = warp_sum(v);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) buf[w] = v;
+  __syncthreads();
+  V s = V(0);
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (unsigned)nw ? buf[threadIdx.x] : V(0);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) buf[0] = s;
+  }
+  __syncthreads();
+  s = buf[0];
+  __syncthreads();
+  return s;
+}
+
+#define MSY_CK(x)                                                                   \
+  do {                                                                              \
+    cudaError_t e__ = (x);                                                          \
+    if (e__ != cudaSuccess) {                                                       \
+      fprintf(stderr, "mpsylv_b200: CUDA error %s at %s:%d\n", cudaGetErrorString(e__), __FILE__, __LINE__); \
+      return -100 - (int)e__;                                                       \
+    }                                                                               \
+  } while (0)
+
+#define MSY_LAUNCH_CK() MSY_CK(cudaGetLastError())
+
+__host__ __device__ static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
+
+// bump allocator over the caller-owned workspace (no cudaMalloc on the hot path)
+struct Arena {
+  char* base;
+  size_t size, off;
+  bool dry;  // sizing pass: count bytes only
+  Arena(void* b, size_t s) : base((char*)b), size(s), off(0), dry(b == nullptr) {}
+  template <class T>
+  T* get(size_t n) {
+    size_t a = (off + 255) & ~(size_t)255;
+    off = a + n * sizeof(T);
+    if (dry) return (T*)(uintptr_t)(0x1000 + a);  // never dereferenced
+    if (off > size) return nullptr;
+    return (T*)(base + a);
+  }
+  bool ok() const { return dry || off <= size; }
+};
+
+}  // namespace msy

@@ -1,0 +1,267 @@
+// hessenberg.cuh -- blocked Householder Hessenberg reduction H = Q0^H A Q0 (large m).
+//
+// Replaces the reference's unblocked `_hessenberg` (pkg/src/mpsylv/linalg.py:446-464,
+// reflectors from `_make_reflector` linalg.py:276-292) for matrices above the
+// one-CTA size.  Panel algorithm (compact-WY, Q_panel = I - V T V^H):
+//   per panel column c = k+i:
+//     hess_col_kernel (1 CTA): finish Y[:, i-1] = tau (A v - Y (V^H v)) and
+//        T[:, i-1], apply the panel's earlier reflectors to column c (right:
+//        -Y V[c,:]^H, left: -V T^H V^H a_c), generate reflector i;
+//     hess_gemv_kernel (grid): A[:, c+1:m] v_i  (the BLAS-2 half, HBM/L2 bound)
+//   per panel: trailing updates as GEMMs (right: -Y V^H; left: -V T^H V^H A).
+// Q0 is formed afterwards by backward blocked accumulation (form_q).
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace msy {
+
+constexpr int HESS_NB = 32;     // panel width
+constexpr int HESS_CHUNK = 256;  // gemv column chunk
+constexpr int HESS_TPB = 1024;
+
+// V: m x m buffer (column c = reflector of column c, zero above row c+1)
+// Y: m x NB, T: NB x NB (this panel), part: nch x m partial gemv sums,
+// tau: per-column taus (length m).
+template <class S>
+__global__ void __launch_bounds__(HESS_TPB) hess_col_kernel(int m, S* A, int lda, int k, int i, int nbp, S* V,
+                                                            int ldv, S* Y, int ldy, S* T, int ldt, const S* part,
+                                                            int nch, S* tau) {
+  typedef typename tr<S>::R R;
+  __shared__ S u[HESS_NB];
+  __shared__ S w[HESS_NB];
+  __shared__ S redS[HESS_NB][HESS_TPB / 32];
+  __shared__ R redR[HESS_TPB / 32];
+  __shared__ S sh_beta, sh_tau, sh_scal;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int c = k + i;
+
+  // ---- finish Y[:, i-1] and T[:, i-1] ----
+  if (i > 0) {
+    const int j = i - 1, cj = k + j;
+    const S* vj = V + (size_t)cj * ldv;
+    // u[q] = V[:, q]^H v_j, q < j (rows cj+1..m-1 are the only nonzeros of v_j)
+    for (int q = 0; q < j; q++) {
+      const S* vq = V + (size_t)(k + q) * ldv;
+      S s = S(0);
+      for (int r = cj + 1 + tid; r < m; r += nt) s = fmacc(vq[r], vj[r], s);
+      s = warp_sum(s);
+      if (lane == 0) redS[q][wid] = s;
+    }
+    __syncthreads();
+    if (tid < j) {
+      S s = S(0);
+      for (int q = 0; q < nw; q++) s += redS[tid][q];
+      u[tid] = s;
+    }
+    __syncthreads();
+    S tj = tau[cj];
+    for (int r = tid; r < m; r += nt) {
+      S y = S(0);
+      for (int ch = 0; ch < nch; ch++) y += part[(size_t)ch * m + r];
+      for (int q = 0; q < j; q++) y = y - Y[r + (size_t)q * ldy] * u[q];
+      Y[r + (size_t)j * ldy] = tj * y;
+    }
+    if (tid < j) {  // T[0:j, j] = -tau_j T[0:j,0:j] u
+      S s = S(0);
+      for (int q = tid; q < j; q++) s = fmac(T[tid + q * ldt], u[q], s);
+      T[tid + j * ldt] = -(tj * s);
+    }
+    if (tid == 0) T[j + j * ldt] = tj;
+    __syncthreads();
+  }
+  if (i >= nbp) return;
+
+  S* ac = A + (size_t)c * lda;
+  // ---- right ops of reflectors 0..i-1 on column c (all rows) ----
+  if (i > 0) {
+    for (int r = tid; r < m; r += nt) {
+      S a = ac[r];
+      for (int q = 0; q < i; q++) a = a - Y[r + (size_t)q * ldy] * conj(V[c + (size_t)(k + q) * ldv]);
+      ac[r] = a;
+    }
+    __syncthreads();
+    // ---- left ops: a[k+1:m] -= V T^H (V^H a) ----
+    for (int q = 0; q < i; q++) {
+      const S* vq = V + (size_t)(k + q) * ldv;
+      S s = S(0);
+      for (int r = k + q + 1 + tid; r < m; r += nt) s = fmacc(vq[r], ac[r], s);
+      s = warp_sum(s);
+      if (lane == 0) redS[q][wid] = s;
+    }
+    __syncthreads();
+    if (tid < i) {
+      S s = S(0);
+      for (int q = 0; q < nw; q++) s += redS[tid][q];
+      u[tid] = s;
+    }
+    __syncthreads();
+    if (tid < i) {  // w = T^H u  (T upper => T^H lower)
+      S s = S(0);
+      for (int q = 0; q <= tid; q++) s = fmacc(T[q + tid * ldt], u[q], s);
+      w[tid] = s;
+    }
+    __syncthreads();
+    for (int r = k + 1 + tid; r < m; r += nt) {
+      S a = ac[r];
+      for (int q = 0; q < i; q++) a = a - V[r + (size_t)(k + q) * ldv] * w[q];
+      ac[r] = a;
+    }
+    __syncthreads();
+  }
+  // ---- reflector for x = a[c+1:m] ----
+  {
+    R s = 0;
+    for (int r = c + 2 + tid; r < m; r += nt) s += abs2(ac[r]);
+    s = warp_sum(s);
+    if (lane == 0) redR[wid] = s;
+    __syncthreads();
+    if (tid == 0) {
+      R t = 0;
+      for (int q = 0; q < nw; q++) t += redR[q];
+      S x0 = ac[c + 1];
+      if (t == R(0) && im(x0) == R(0)) {
+        sh_tau = S(0); sh_beta = x0; sh_scal = S(0);
+      } else {
+        R nrm = sqrt(abs2(x0) + t);
+        R b = re(x0) >= R(0) ? -nrm : nrm;
+        sh_beta = mk<S>(b);
+        sh_tau = (mk<S>(b) - x0) / mk<S>(b);
+        sh_scal = S(1) / (x0 - mk<S>(b));
+      }
+    }
+    __syncthreads();
+    S* vc = V + (size_t)c * ldv;
+    S scal = sh_scal;
+    for (int r = c + 1 + tid; r < m; r += nt) {
+      vc[r] = (r == c + 1) ? S(1) : ac[r] * scal;
+      ac[r] = (r == c + 1) ? sh_beta : S(0);
+    }
+    if (tid == 0) tau[c] = sh_tau;
+  }
+}
+
+// part[ch][r] = sum over columns q in chunk ch (q > c) of A[r, q] v[q]
+template <class S>
+__global__ void __launch_bounds__(256) hess_gemv_kernel(int m, const S* __restrict__ A, int lda, int c0,
+                                                        const S* __restrict__ v, S* part) {
+  const int r = blockIdx.x * 256 + threadIdx.x;
+  const int ch = blockIdx.y;
+  const int q0 = c0 + ch * HESS_CHUNK, q1 = min(m, q0 + HESS_CHUNK);
+  __shared__ S vs[HESS_CHUNK];
+  for (int q = q0 + threadIdx.x; q < q1; q += 256) vs[q - q0] = v[q];
+  __syncthreads();
+  if (r >= m) return;
+  S s0 = S(0), s1 = S(0), s2 = S(0), s3 = S(0);
+  int q = q0;
+  for (; q + 3 < q1; q += 4) {
+    s0 = fmac(A[r + (size_t)q * lda], vs[q - q0], s0);
+    s1 = fmac(A[r + (size_t)(q + 1) * lda], vs[q + 1 - q0], s1);
+    s2 = fmac(A[r + (size_t)(q + 2) * lda], vs[q + 2 - q0], s2);
+    s3 = fmac(A[r + (size_t)(q + 3) * lda], vs[q + 3 - q0], s3);
+  }
+  for (; q < q1; q++) s0 = fmac(A[r + (size_t)q * lda], vs[q - q0], s0);
+  part[(size_t)ch * m + r] = (s0 + s1) + (s2 + s3);
+}
+
+template <class S>
+__global__ void set_identity_kernel(int m, int n, S* M, int ld) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i < m) M[i + (size_t)j * ld] = (i == j) ? S(1) : S(0);
+}
+template <class S>
+__global__ void zero_kernel(size_t n, S* p) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = S(0);
+}
+template <class S>
+__global__ void clear_below_sub_kernel(int m, S* A, int lda) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i < m && i > j + 1) A[i + (size_t)j * lda] = S(0);
+}
+
+template <class S>
+struct HessWs {
+  S *V, *Y, *T, *part, *tau, *W1, *W2;
+  static void carve(Arena& ar, int m, HessWs& w) {
+    w.V = ar.get<S>((size_t)m * m);
+    w.Y = ar.get<S>((size_t)m * HESS_NB);
+    w.T = ar.get<S>((size_t)HESS_NB * (m + HESS_NB));  // one NB x NB T per panel
+    w.part = ar.get<S>((size_t)cdiv(m, HESS_CHUNK) * m);
+    w.tau = ar.get<S>((size_t)m);
+    w.W1 = ar.get<S>((size_t)HESS_NB * m);
+    w.W2 = ar.get<S>((size_t)HESS_NB * m);
+  }
+};
+
+// In place: A -> H (upper Hessenberg), Q (m x m) = Q0.
+template <class S>
+int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaStream_t st) {
+  const int ldv = m, ldy = m, ldt = HESS_NB;
+  zero_kernel<S><<<cdiv((size_t)m * m, 256), 256, 0, st>>>((size_t)m * m, w.V);
+  MSY_LAUNCH_CK();
+  const int last = m - 3;  // last column that gets a reflector
+  int np = 0;
+  for (int k = 0; k <= last; k += HESS_NB, np++) {
+    const int nbp = min(HESS_NB, last - k + 1);
+    S* T = w.T + (size_t)np * HESS_NB * ldt;
+    zero_kernel<S><<<cdiv(HESS_NB * HESS_NB, 256), 256, 0, st>>>((size_t)HESS_NB * HESS_NB, T);
+    for (int i = 0; i < nbp; i++) {
+      const int c = k + i;
+      int nch = i > 0 ? cdiv(m - c, HESS_CHUNK) : 0;  // gemv for reflector i-1 covered columns c..m-1
+      hess_col_kernel<S><<<1, HESS_TPB, 0, st>>>(m, A, lda, k, i, nbp, w.V, ldv, w.Y, ldy, T, ldt, w.part, nch, w.tau);
+      MSY_LAUNCH_CK();
+      // gemv with v_i over columns c+1..m-1
+      int nchn = cdiv(m - (c + 1), HESS_CHUNK);
+      hess_gemv_kernel<S><<<dim3(cdiv(m, 256), nchn), 256, 0, st>>>(m, A, lda, c + 1, w.V + (size_t)c * ldv, w.part);
+      MSY_LAUNCH_CK();
+    }
+    {  // finish Y[:, nbp-1]
+      int c = k + nbp;
+      int nch = cdiv(m - c, HESS_CHUNK);
+      hess_col_kernel<S><<<1, HESS_TPB, 0, st>>>(m, A, lda, k, nbp, nbp, w.V, ldv, w.Y, ldy, T, ldt, w.part, nch,
+                                                 w.tau);
+      MSY_LAUNCH_CK();
+    }
+    const int c1 = k + nbp;  // first trailing column
+    const int nc = m - c1;
+    if (nc > 0) {
+      const S* Vp = w.V + (size_t)k * ldv;  // columns k..k+nbp-1
+      // right: A[:, c1:m] -= Y V[c1:m, :]^H
+      int rc = gemm<S>('N', 'C', m, nc, nbp, S(-1), w.Y, ldy, Vp + c1, ldv, S(1), A + (size_t)c1 * lda, lda, st);
+      if (rc) return rc;
+      // left: W1 = V[k+1:m,:]^H A[k+1:m, c1:m]; W2 = T^H W1; A -= V W2
+      rc = gemm<S>('C', 'N', nbp, nc, m - k - 1, S(1), Vp + (k + 1), ldv, A + (k + 1) + (size_t)c1 * lda, lda, S(0),
+                   w.W1, HESS_NB, st);
+      if (rc) return rc;
+      rc = gemm<S>('C', 'N', nbp, nc, nbp, S(1), T, ldt, w.W1, HESS_NB, S(0), w.W2, HESS_NB, st);
+      if (rc) return rc;
+      rc = gemm<S>('N', 'N', m - k - 1, nc, nbp, S(-1), Vp + (k + 1), ldv, w.W2, HESS_NB, S(1),
+                   A + (k + 1) + (size_t)c1 * lda, lda, st);
+      if (rc) return rc;
+    }
+  }
+  clear_below_sub_kernel<S><<<dim3(cdiv(m, 256), m), 256, 0, st>>>(m, A, lda);
+  MSY_LAUNCH_CK();
+  // ---- form Q0 = P_0 ... P_{m-3} by backward panel accumulation ----
+  set_identity_kernel<S><<<dim3(cdiv(m, 256), m), 256, 0, st>>>(m, m, Q, ldq);
+  MSY_LAUNCH_CK();
+  for (int p = np - 1; p >= 0; p--) {
+    int k = p * HESS_NB;
+    int nbp = min(HESS_NB, last - k + 1);
+    const S* Vp = w.V + (size_t)k * ldv;
+    const S* T = w.T + (size_t)p * HESS_NB * ldt;
+    int r0 = k + 1, nr = m - r0;
+    // Q[r0:m, r0:m] -= V T (V^H Q[r0:m, r0:m])
+    int rc = gemm<S>('C', 'N', nbp, nr, nr, S(1), Vp + r0, ldv, Q + r0 + (size_t)r0 * ldq, ldq, S(0), w.W1, HESS_NB,
+                     st);
+    if (rc) return rc;
+    rc = gemm<S>('N', 'N', nbp, nr, nbp, S(1), T, ldt, w.W1, HESS_NB, S(0), w.W2, HESS_NB, st);
+    if (rc) return rc;
+    rc = gemm<S>('N', 'N', nr, nr, nbp, S(-1), Vp + r0, ldv, w.W2, HESS_NB, S(1), Q + r0 + (size_t)r0 * ldq, ldq, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+}  // namespace msy

@@ -1,0 +1,376 @@
+// multishift.cuh -- small-bulge multishift QR for Hessenberg matrices above the one-CTA size.
+//
+// Replaces the reference's single-shift sweep loop `schur` (pkg/src/mpsylv/linalg.py:518-577,
+// rotations `_givens`/`_rot_rows`/`_rot_cols` :467-499) for large m.  B200 design:
+//   * a chain of nb double-shift bulges (3-element reflectors, bulges 4 rows apart,
+//     one warp per bulge, all bulges of a step in parallel) is chased through a
+//     W x W diagonal window held in shared memory by ONE CTA (chase_kernel);
+//     the window's accumulated orthogonal factor Z stays in smem too;
+//   * the off-window parts of H (rows to the right, columns above) and the Schur
+//     vectors U are updated with Z as in-place GEMMs over many CTAs (apply_z_kernel);
+//   * deflation uses the reference's criterion (linalg.py:541-544); converged
+//     trailing 1x1 (and, real, 2x2) blocks are skipped, complex 2x2 blocks are
+//     split in scan_kernel; blocks of order <= NMIN finish in schur_small_kernel.
+//   * shifts: eigenvalues of the trailing ns x ns block (schur_small_kernel in
+//     eigenvalue mode), exceptional shifts after 6 stagnant sweeps.
+#pragma once
+#include "common.cuh"
+#include "schur_small.cuh"
+
+namespace msy {
+
+template <class S> struct MsCfg;
+template <> struct MsCfg<float> { static constexpr int W = 128, NB = 16; };
+template <> struct MsCfg<double> { static constexpr int W = 96, NB = 12; };
+template <> struct MsCfg<cfloat> { static constexpr int W = 96, NB = 12; };
+template <> struct MsCfg<cdouble> { static constexpr int W = 64, NB = 8; };
+
+// ---------------------------------------------------------------------------
+// window chase
+template <class S>
+__global__ void __launch_bounds__(512) chase_kernel(S* H, int ldh, int lo, int hi, int nb,
+                                                    const typename tr<S>::R* __restrict__ shifts, int ws, int we,
+                                                    int t0, int t1, S* Zg) {
+  typedef typename tr<S>::R R;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nw = we - ws;
+  const int ld = nw + 1;
+  S* Hw = (S*)smem_raw;
+  S* Zw = Hw + (size_t)ld * nw;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+#define HW(i, j) Hw[(i) + (j) * ld]
+#define ZW(i, j) Zw[(i) + (j) * ld]
+  for (int e = tid; e < nw * nw; e += nt) {
+    int i = e % nw, j = e / nw;
+    HW(i, j) = H[(ws + i) + (size_t)(ws + j) * ldh];
+    ZW(i, j) = (i == j) ? S(1) : S(0);
+  }
+  __syncthreads();
+  const int j = warp;  // bulge handled by this warp
+  for (int t = t0; t < t1; t++) {
+    const int p = lo - 1 + t - 4 * j;  // global position
+    const bool act = (j < nb) && (p >= lo - 1) && (p <= hi - 2);
+    S tau = S(0), v1 = S(0), v2 = S(0), beta = S(0);
+    int nr = 0, pl = p - ws;  // window-local position
+    if (act) {
+      nr = (hi - p) >= 3 ? 3 : 2;
+      if (lane == 0) {
+        S x0, x1, x2;
+        if (p == lo - 1) {
+          const R* w4 = shifts + 4 * j;
+          int l = lo - ws;
+          shift_poly<S>(HW(l, l), HW(l + 1, l), HW(l, l + 1), HW(l + 1, l + 1), (lo + 2 <= hi) ? HW(l + 2, l + 1) : S(0),
+                        w4, x0, x1, x2);
+        } else {
+          x0 = HW(pl + 1, pl); x1 = HW(pl + 2, pl); x2 = nr > 2 ? HW(pl + 3, pl) : S(0);
+        }
+        make_refl3<S>(nr, x0, x1, x2, beta, tau, v1, v2);
+      }
+      tau = shfl(tau, 0); v1 = shfl(v1, 0); v2 = shfl(v2, 0); beta = shfl(beta, 0);
+      // phase A: left op on rows pl+1..pl+nr, window columns (p+1 or lo)..we-1
+      if (!iszero(tau)) {
+        S ctau = conj(tau);
+        const int c0 = pl + 1;
+        for (int c = c0 + lane; c < nw; c += 32) {
+          S h0 = HW(pl + 1, c), h1 = HW(pl + 2, c), h2 = nr > 2 ? HW(pl + 3, c) : S(0);
+          S w = fmacc(v1, h1, h0);
+          if (nr > 2) w = fmacc(v2, h2, w);
+          w = ctau * w;
+          HW(pl + 1, c) = h0 - w;
+          HW(pl + 2, c) = h1 - v1 * w;
+          if (nr > 2) HW(pl + 3, c) = h2 - v2 * w;
+        }
+      }
+      if (p >= lo && lane == 0) {
+        HW(pl + 1, pl) = beta;
+        HW(pl + 2, pl) = S(0);
+        if (nr > 2) HW(pl + 3, pl) = S(0);
+      }
+    }
+    __syncthreads();
+    if (act && !iszero(tau)) {
+      // phase B: right op on columns pl+1..pl+nr, window rows 0..min(p+4,hi)-ws; Z all rows
+      const int rmax = ((p + 4 < hi) ? p + 4 : hi) - ws;
+      for (int e = lane; e < nw + rmax + 1; e += 32) {
+        S* M;
+        int r;
+        if (e <= rmax) { M = Hw; r = e; } else { M = Zw; r = e - rmax - 1; }
+        S h0 = M[r + (pl + 1) * ld], h1 = M[r + (pl + 2) * ld], h2 = nr > 2 ? M[r + (pl + 3) * ld] : S(0);
+        S w = fmac(h1, v1, h0);
+        if (nr > 2) w = fmac(h2, v2, w);
+        w = tau * w;
+        M[r + (pl + 1) * ld] = h0 - w;
+        M[r + (pl + 2) * ld] = h1 - w * conj(v1);
+        if (nr > 2) M[r + (pl + 3) * ld] = h2 - w * conj(v2);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nw * nw; e += nt) {
+    int i = e % nw, jj = e / nw;
+    H[(ws + i) + (size_t)(ws + jj) * ldh] = HW(i, jj);
+    Zg[i + (size_t)jj * nw] = ZW(i, jj);
+  }
+#undef HW
+#undef ZW
+}
+
+// ---------------------------------------------------------------------------
+// in-place application of a small orthogonal Z (nz x nz, ld nz):
+//   region L: H[r0:r0+nz, cL0:cL1] <- Z^H * (.)       (tiles of 32 columns)
+//   region R: H[0:rR1, c0:c0+nz]   <- (.) * Z          (tiles of 32 rows)
+//   region U: U[0:mU, c0:c0+nz]    <- (.) * Z
+template <class S>
+__global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restrict__ Zg, S* H, int ldh, int r0,
+                                                      int cL0, int cL1, int rR1, S* U, int ldu, int mU) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ldz = nz + 1;
+  S* Zs = (S*)smem_raw;
+  S* Ts = Zs + (size_t)ldz * nz;  // tile: nz x 33 (L) or 32 x (nz+1) (R)
+  const int tid = threadIdx.x;
+  const int ntL = cdiv(cL1 - cL0, 32), ntR = cdiv(rR1, 32), ntU = cdiv(mU, 32);
+  int b = blockIdx.x;
+  for (int e = tid; e < nz * nz; e += 256) Zs[(e % nz) + (e / nz) * ldz] = Zg[e];
+  if (b < ntL) {
+    const int c0 = cL0 + b * 32, nc = min(32, cL1 - c0);
+    const int ldt = nz + 1;  // tile stored transposed-free: Ts[r + c*ldt]
+    for (int e = tid; e < nz * 32; e += 256) {
+      int r = e % nz, c = e / nz;
+      Ts[r + c * ldt] = c < nc ? H[(r0 + r) + (size_t)(c0 + c) * ldh] : S(0);
+    }
+    __syncthreads();
+    // out[i, c] = sum_r conj(Z[r, i]) T[r, c]; thread: rows i = tr + 32a, cols c = 4 tc + q
+    const int tr_ = tid & 31, tc = tid >> 5;
+    S acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[a][q] = S(0);
+    for (int r = 0; r < nz; r++) {
+      S z[4], t[4];
+#pragma unroll
+      for (int a = 0; a < 4; a++) { int i = tr_ + 32 * a; z[a] = i < nz ? conj(Zs[r + i * ldz]) : S(0); }
+#pragma unroll
+      for (int q = 0; q < 4; q++) t[q] = Ts[r + (4 * tc + q) * ldt];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[a][q] = fmac(z[a], t[q], acc[a][q]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+      int i = tr_ + 32 * a;
+      if (i >= nz) continue;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        int c = 4 * tc + q;
+        if (c < nc) H[(r0 + i) + (size_t)(c0 + c) * ldh] = acc[a][q];
+      }
+    }
+    return;
+  }
+  b -= ntL;
+  S* M;
+  int ldm, rbase, nrows;
+  if (b < ntR) { M = H; ldm = ldh; rbase = b * 32; nrows = min(32, rR1 - rbase); }
+  else { b -= ntR; if (b >= ntU) return; M = U; ldm = ldu; rbase = b * 32; nrows = min(32, mU - rbase); }
+  const int c0 = (M == H) ? (r0) : r0;  // region columns start at r0 (== window start)
+  const int ldt = nz + 1;               // Ts[r + c*32]: 32 rows x nz cols
+  for (int e = tid; e < 32 * nz; e += 256) {
+    int r = e % 32, c = e / 32;
+    Ts[r + c * 32] = r < nrows ? M[(rbase + r) + (size_t)(c0 + c) * ldm] : S(0);
+  }
+  (void)ldt;
+  __syncthreads();
+  // out[r, j] = sum_i T[r, i] Z[i, j]; thread: rows r = 4g + q, cols j = lane + 32a
+  const int lane = tid & 31, g = tid >> 5;
+  S acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) acc[a][q] = S(0);
+  for (int i = 0; i < nz; i++) {
+    S z[4], t[4];
+#pragma unroll
+    for (int a = 0; a < 4; a++) { int jj = lane + 32 * a; z[a] = jj < nz ? Zs[i + jj * ldz] : S(0); }
+#pragma unroll
+    for (int q = 0; q < 4; q++) t[q] = Ts[(4 * g + q) + i * 32];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[a][q] = fmac(t[q], z[a], acc[a][q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    int r = 4 * g + q;
+    if (r >= nrows) continue;
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+      int jj = lane + 32 * a;
+      if (jj < nz) M[(rbase + r) + (size_t)(c0 + jj) * ldm] = acc[a][q];
+    }
+  }
+}
+
+template <class S>
+static size_t applyz_smem(int nz) {
+  return ((size_t)(nz + 1) * nz + (size_t)(nz + 1) * 33 + 32 * (size_t)nz) * sizeof(S) + 64;
+}
+
+// Apply Z (window [w0, w0+nz)) to everything outside the window's diagonal block.
+template <class S>
+int apply_z(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int w0, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    MSY_CK(cudaFuncSetAttribute(apply_z_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)applyz_smem<S>(128)));
+    attr = true;
+  }
+  if (nz > 128) return -4;
+  const int cL0 = w0 + nz, cL1 = m, rR1 = w0;
+  int nblk = cdiv(cL1 - cL0, 32) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
+  if (nblk == 0) return 0;
+  apply_z_kernel<S><<<nblk, 256, applyz_smem<S>(nz), st>>>(nz, Z, H, ldh, w0, cL0, cL1, rR1, U, ldu, U ? m : 0);
+  MSY_LAUNCH_CK();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// deflation scan: zero negligible subdiagonals in [1, hi]; skip converged trailing
+// blocks (1x1; real 2x2; complex 2x2 after a splitting rotation); report the
+// new hi and the start lo of its unreduced block.  out[0] = hi', out[1] = lo.
+template <class S>
+__global__ void __launch_bounds__(1024) scan_kernel(int m, S* H, int ldh, S* U, int ldu, int hi, int* out) {
+  typedef typename tr<S>::R R;
+  const R u = tr<S>::u();
+  __shared__ int s_i, s_act;
+  const int tid = threadIdx.x, nt = blockDim.x;
+#define HH(i, j) H[(i) + (size_t)(j) * ldh]
+  for (int k = 1 + tid; k <= hi; k += nt) {
+    S h = HH(k, k - 1);
+    if (!iszero(h) && absv(h) <= u * (absv(HH(k - 1, k - 1)) + absv(HH(k, k)))) HH(k, k - 1) = S(0);
+  }
+  __syncthreads();
+  if (tid == 0) s_i = hi;
+  __syncthreads();
+  while (true) {
+    if (tid == 0) {
+      int i = s_i;
+      s_act = 0;
+      while (i >= 0) {
+        if (i == 0) { i = -1; break; }
+        if (iszero(HH(i, i - 1))) { i -= 1; continue; }
+        if (i == 1 || iszero(HH(i - 1, i - 2))) {
+          if (tr<S>::cx) { s_act = 1; break; }
+          i -= 2;
+          continue;
+        }
+        break;
+      }
+      s_i = i;
+    }
+    __syncthreads();
+    if (!s_act) break;
+    // complex 2x2 split of [i-1, i] (see schur_small_kernel, mode 2)
+    const int i = s_i, l = i - 1;
+    R w4[4];
+    S a = HH(l, l), b = HH(l, i), c = HH(i, l), d = HH(i, i);
+    eig2<S>(a, b, c, d, w4);
+    S lam = mk<S>(w4[0], w4[1]);
+    S va = lam - d, vb = c, wa = b, wb = lam - a;
+    if (abs2(wa) + abs2(wb) > abs2(va) + abs2(vb)) { va = wa; vb = wb; }
+    R nv = sqrt(abs2(va) + abs2(vb));
+    S g11 = va / mk<S>(nv), g21 = vb / mk<S>(nv);
+    S g12 = -conj(g21), g22 = conj(g11);
+    __syncthreads();
+    for (int j = l + tid; j < m; j += nt) {
+      S h1 = HH(l, j), h2 = HH(i, j);
+      HH(l, j) = fmacc(g11, h1, conj(g21) * h2);
+      HH(i, j) = fmacc(g12, h1, conj(g22) * h2);
+    }
+    __syncthreads();
+    for (int e = tid; e < (i + 1) + m; e += nt) {
+      S* M;
+      int r;
+      size_t ldx;
+      if (e <= i) { M = H; r = e; ldx = ldh; } else { M = U; r = e - i - 1; ldx = ldu; }
+      S c1 = M[r + l * ldx], c2 = M[r + i * ldx];
+      M[r + l * ldx] = c1 * g11 + c2 * g21;
+      M[r + i * ldx] = c1 * g12 + c2 * g22;
+    }
+    __syncthreads();
+    if (tid == 0) { HH(i, l) = S(0); s_i = i - 2; }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int i = s_i, lo = 0;
+    for (int k = i; k >= 1; k--)
+      if (iszero(HH(k, k - 1))) { lo = k; break; }
+    out[0] = i;
+    out[1] = i >= 0 ? lo : 0;
+  }
+#undef HH
+}
+
+// build per-bulge shift quadruples (sr1, si1, sr2, si2) from eigenvalues (wr, wi)
+// of the trailing block; exceptional shifts from the trailing subdiagonals.
+template <class S>
+__global__ void pair_shifts_kernel(int ns, const typename tr<S>::R* wr, const typename tr<S>::R* wi, int nb,
+                                   typename tr<S>::R* out, int exceptional, const S* H, int ldh, int lo, int hi,
+                                   int* nb_out) {
+  typedef typename tr<S>::R R;
+  if (threadIdx.x != 0) return;
+  int b = 0;
+  if (exceptional) {
+    for (int k = 0; k < nb; k++) {
+      int i = hi - 2 * k;
+      if (i - 2 < lo) i = hi;
+      R ss = absv(H[i + (size_t)(i - 1) * ldh]) + absv(H[(i - 1) + (size_t)(i - 2) * ldh]);
+      S aa = mk<S>(R(0.75) * ss) + H[i + (size_t)i * ldh];
+      R w4[4];
+      eig2<S>(aa, mk<S>(ss), mk<S>(R(-0.4375) * ss), aa, w4);
+      for (int q = 0; q < 4; q++) out[4 * b + q] = w4[q];
+      b++;
+    }
+    *nb_out = b;
+    return;
+  }
+  if (tr<S>::cx) {
+    for (int k = 0; k + 1 < ns && b < nb; k += 2) {
+      out[4 * b] = wr[k]; out[4 * b + 1] = wi[k]; out[4 * b + 2] = wr[k + 1]; out[4 * b + 3] = wi[k + 1];
+      b++;
+    }
+  } else {
+    int pend = -1;
+    for (int k = 0; k < ns && b < nb; k++) {
+      if (wi[k] != R(0)) {  // conjugate pair occupies k, k+1
+        if (k + 1 < ns) {
+          out[4 * b] = wr[k]; out[4 * b + 1] = wi[k]; out[4 * b + 2] = wr[k + 1]; out[4 * b + 3] = wi[k + 1];
+          b++;
+        }
+        k++;
+        continue;
+      }
+      if (pend < 0) { pend = k; continue; }
+      out[4 * b] = wr[pend]; out[4 * b + 1] = 0; out[4 * b + 2] = wr[k]; out[4 * b + 3] = 0;
+      b++;
+      pend = -1;
+    }
+  }
+  if (b == 0) {  // nothing pairable: fall back to the trailing diagonal entry
+    R h = re(H[hi + (size_t)hi * ldh]), hi_ = im(H[hi + (size_t)hi * ldh]);
+    out[0] = h; out[1] = hi_; out[2] = h; out[3] = hi_;
+    b = 1;
+  }
+  for (int k = b; k < nb; k++)
+    for (int q = 0; q < 4; q++) out[4 * k + q] = out[4 * (k % b) + q];
+  *nb_out = b;
+}
+
+template <class S>
+__global__ void copy_block_kernel(int n, const S* A, int lda, S* B, int ldb) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i < n) B[i + (size_t)j * ldb] = A[i + (size_t)j * lda];
+}
+
+}  // namespace msy

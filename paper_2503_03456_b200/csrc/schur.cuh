@@ -1,0 +1,157 @@
+// schur.cuh -- A = U T U^H on the device (replaces `schur`, pkg/src/mpsylv/linalg.py:518-577).
+//
+//   m <= NMIN : schur_small_kernel (Hessenberg + double-shift QR in one CTA's smem)
+//   m >  NMIN : hessenberg_blocked, then a host-driven loop of
+//               scan (deflation) -> shifts (trailing block eigenvalues) -> multishift sweep
+//               (window chase + Z application), finishing blocks <= NMIN in one CTA.
+// Status: 0 ok, 3 = iteration limit (IterationLimitError, linalg.py:552-554).
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+#include "hessenberg.cuh"
+#include "multishift.cuh"
+#include "schur_small.cuh"
+
+namespace msy {
+
+template <class S>
+struct SchurWs {
+  typedef typename tr<S>::R R;
+  HessWs<S> hw;
+  S* Z;       // 128 x 128
+  S* sblk;    // trailing block copy
+  R* wr;
+  R* wi;
+  R* shifts;  // 4 per bulge
+  int* dinfo; // small device ints
+  static void carve(Arena& ar, int m, SchurWs& w) {
+    if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
+    w.Z = ar.get<S>(128 * 128);
+    w.sblk = ar.get<S>(128 * 128);
+    w.wr = ar.get<R>(256);
+    w.wi = ar.get<R>(256);
+    w.shifts = ar.get<R>(4 * 64);
+    w.dinfo = ar.get<int>(64);
+  }
+};
+
+struct SchurStats {
+  int status, sweeps, small_calls, windows;
+};
+
+template <class S>
+int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const typename tr<S>::R* shifts, S* Zbuf,
+             cudaStream_t st, int* nwin) {
+  constexpr int W = MsCfg<S>::W;
+  static bool attr = false;
+  const size_t smem_max = (size_t)2 * (W + 1) * W * sizeof(S);
+  if (!attr) {
+    MSY_CK(cudaFuncSetAttribute(chase_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+    attr = true;
+  }
+  const int span = hi - lo;
+  const long Tn = 4L * (nb - 1) + span;
+  auto Lf = [&](long t) {
+    long jt = std::min<long>(nb - 1, t / 4);
+    long P = lo - 1 + t - 4 * jt;
+    return (int)std::max<long>(P, lo);
+  };
+  auto Uf = [&](long t) {
+    long x = t - (span - 1);
+    long jh = x > 0 ? (x + 3) / 4 : 0;
+    long P = lo - 1 + t - 4 * jh;
+    return (int)std::min<long>(P + 4, hi);
+  };
+  long t = 0;
+  while (t < Tn) {
+    int ws = Lf(t);
+    int we = std::min(ws + W, hi + 1);
+    long t1 = t;
+    while (t1 < Tn && Uf(t1) <= we - 1) t1++;
+    if (t1 == t) return -5;
+    int nw = we - ws;
+    chase_kernel<S><<<1, 32 * std::max(nb, 4), (size_t)2 * (nw + 1) * nw * sizeof(S), st>>>(H, ldh, lo, hi, nb, shifts,
+                                                                                         ws, we, (int)t, (int)t1, Zbuf);
+    MSY_LAUNCH_CK();
+    int rc = apply_z<S>(m, nw, Zbuf, H, ldh, U, ldu, ws, st);
+    if (rc) return rc;
+    if (nwin) (*nwin)++;
+    t = t1;
+  }
+  return 0;
+}
+
+// In place: A (m x m, lda) -> T; U (m x m, ldu) = Schur vectors.
+template <class S>
+int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_t st, SchurStats* stats) {
+  typedef typename tr<S>::R R;
+  constexpr int NMIN = SmallCfg<S>::NMAX;
+  SchurStats loc = {0, 0, 0, 0};
+  if (m <= NMIN) {
+    int rc = schur_small_launch<S>(m, A, lda, U, ldu, SS_HESS | SS_WANTZ, nullptr, nullptr, w.dinfo, st);
+    if (rc) return rc;
+    int hinfo[2];
+    MSY_CK(cudaMemcpyAsync(hinfo, w.dinfo, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
+    MSY_CK(cudaStreamSynchronize(st));
+    loc.status = hinfo[0];
+    loc.sweeps = hinfo[1];
+    loc.small_calls = 1;
+    if (stats) *stats = loc;
+    return 0;
+  }
+  int rc = hessenberg_blocked<S>(m, A, lda, U, ldu, w.hw, st);
+  if (rc) return rc;
+  int hi = m - 1, stag = 0, last_hi = m;
+  const int limit = 30 * m;
+  while (true) {
+    scan_kernel<S><<<1, 1024, 0, st>>>(m, A, lda, U, ldu, hi, w.dinfo);
+    MSY_LAUNCH_CK();
+    int hinfo[4];
+    MSY_CK(cudaMemcpyAsync(hinfo, w.dinfo, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    MSY_CK(cudaStreamSynchronize(st));
+    hi = hinfo[0];
+    int lo = hinfo[1];
+    if (hi < 0) break;
+    if (hi < last_hi) { stag = 0; last_hi = hi; } else stag++;
+    int sz = hi - lo + 1;
+    if (sz <= NMIN) {
+      S* blk = A + lo + (size_t)lo * lda;
+      rc = schur_small_launch<S>(sz, blk, lda, w.Z, sz, SS_WANTZ, nullptr, nullptr, w.dinfo + 8, st);
+      if (rc) return rc;
+      rc = apply_z<S>(m, sz, w.Z, A, lda, U, ldu, lo, st);
+      if (rc) return rc;
+      int sinfo[2];
+      MSY_CK(cudaMemcpyAsync(sinfo, w.dinfo + 8, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      MSY_CK(cudaStreamSynchronize(st));
+      loc.small_calls++;
+      loc.sweeps += sinfo[1];
+      if (sinfo[0]) { loc.status = sinfo[0]; break; }
+      hi = lo - 1;
+      last_hi = hi + 1;
+      stag = 0;
+      if (hi < 0) break;
+      continue;
+    }
+    if (loc.sweeps >= limit) { loc.status = ST_ITERLIMIT; break; }
+    int nb = std::min(MsCfg<S>::NB, std::max(1, (sz - 8) / 8));
+    int ns = 2 * nb;
+    bool exc = (stag > 0 && stag % 6 == 0);
+    if (!exc) {
+      const S* src = A + (hi - ns + 1) + (size_t)(hi - ns + 1) * lda;
+      copy_block_kernel<S><<<dim3(cdiv(ns, 128), ns), 128, 0, st>>>(ns, src, lda, w.sblk, ns);
+      MSY_LAUNCH_CK();
+      rc = schur_small_launch<S>(ns, w.sblk, ns, nullptr, 0, SS_EIGONLY, w.wr, w.wi, w.dinfo + 16, st);
+      if (rc) return rc;
+    }
+    pair_shifts_kernel<S><<<1, 32, 0, st>>>(ns, w.wr, w.wi, nb, w.shifts, exc ? 1 : 0, A, lda, lo, hi, w.dinfo + 24);
+    MSY_LAUNCH_CK();
+    // bulges whose shifts could not be paired reuse the last pair
+    rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, w.shifts, w.Z, st, &loc.windows);
+    if (rc) return rc;
+    loc.sweeps++;
+  }
+  if (stats) *stats = loc;
+  return 0;
+}
+
+}  // namespace msy

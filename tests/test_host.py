@@ -1,0 +1,111 @@
+"""CPU-only checks: the C ABI library loads and exports every symbol the header
+declares, the host-side mirror of the reference API validates like the
+reference, the generators are deterministic, the cost model matches."""
+
+import ctypes as ct
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "mpsylv_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sylv_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2503_03456_b200 import _native
+    from paper_2503_03456_b200.build import build
+    build(verbose=False)
+    lib = ct.CDLL(_native.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 13
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_native.EXPORTS)
+
+
+def test_struct_layouts_match_header():
+    from paper_2503_03456_b200 import _native
+    # sylv_params: 9 ints + a double (aligned) ; sylv_report contains the norms array
+    assert ct.sizeof(_native.Params) == 48
+    assert ct.sizeof(_native.Report) > 8 * _native.MAX_NORMS
+
+
+def test_status_strings_without_gpu():
+    from paper_2503_03456_b200 import _native
+    L = _native.lib()
+    assert L.sylv_version() == 1
+    assert L.sylv_status_string(1) == b"singular_equation"
+    assert L.sylv_status_string(-3) == b"workspace_too_small"
+
+
+def test_workspace_queries_without_gpu():
+    from paper_2503_03456_b200 import _native
+    L = _native.lib()
+    p = _native.Params(m=4096, n=4096, kind=0, complex_data=0, variant=0, low_bits=32, correction_bits=64,
+                       max_iter=20, y0_zero=0, epsilon=4.096e-9)
+    sz = ct.c_size_t()
+    assert L.sylv_workspace_size(ct.byref(p), ct.byref(sz)) == 0
+    assert 1e9 < sz.value < 8e9
+    p.low_bits = 16
+    assert L.sylv_workspace_size(ct.byref(p), ct.byref(sz)) == _native.EUNSUPPORTED
+
+
+def test_config_and_precision_pairs():
+    from paper_2503_03456_b200 import (BFLOAT16, BINARY32, BINARY64, TF32, RefinementConfig,
+                                       UnsupportedPrecisionError)
+    from paper_2503_03456_b200.refinement import _precision_pair
+    assert RefinementConfig(BINARY64, BINARY64).resolve_epsilon(7, 12) == 1e-12 * 12
+    assert RefinementConfig(TF32, BINARY32).resolve_epsilon(5, 5) == 1e4 * BINARY32.unit_roundoff * 5
+    with pytest.raises(ValueError):
+        RefinementConfig(BINARY64, BINARY32)
+    assert RefinementConfig(BINARY32, BINARY64).max_iter == 20
+    assert _precision_pair(RefinementConfig(BINARY32, BINARY64)) == 32
+    assert _precision_pair(RefinementConfig(BINARY64, BINARY64)) == 64
+    for lo in (TF32, BFLOAT16):
+        with pytest.raises(UnsupportedPrecisionError):
+            _precision_pair(RefinementConfig(lo, BINARY64))
+
+
+def test_sylvester_problem_validation(rng):
+    from paper_2503_03456_b200 import DimensionError, SylvesterProblem
+    A = rng.standard_normal((3, 3))
+    with pytest.raises(ValueError):
+        SylvesterProblem(A, A, np.ones((3, 3)), kind="lyapunov")
+    with pytest.raises(DimensionError):
+        SylvesterProblem(A, np.eye(2), np.ones((3, 3)))
+    p = SylvesterProblem(A, A.T, np.ones((3, 3)), kind="lyapunov")
+    assert p.m == 3 and p.n == 3 and p.A.dtype == np.complex128
+
+
+def test_cost_model_matches_reference_table():
+    from paper_2503_03456_b200.costmodel import flops
+    a, b = 2 * 128 ** 3, 128 * 128 * 256
+    f = flops("mp_orth_sylv", 128, 128, 2)
+    assert f.low_flops == 25 * a + b and f.high_flops == 6 * a + 10 * b
+    assert flops("mp_orth_lyap", 10, 10, 1).high_flops == 20 * 1000
+
+
+def test_generators_deterministic_and_shaped():
+    from paper_2503_03456_b200 import problems as P
+    a, b = P.make("c0", 16, seed=0), P.make("c0", 16, seed=0)
+    assert (a.A == b.A).all() and (a.C == b.C).all()
+    c1 = P.make("c1", 12)
+    assert np.allclose(c1.B, c1.A.T) and np.allclose(c1.C, c1.C.T)
+    c2 = P.make("c2", 12, 8)
+    assert np.linalg.norm(c2.A @ c2.X_true + c2.X_true @ c2.B - c2.C) < 1e-12 * np.linalg.norm(c2.C)
+    c3 = P.make("c3", 8)
+    assert c3.is_complex and not c2.is_complex
+    assert (P.make_c4(3, 16).A == P.make_c0(16, 16, 3).A).all()
+
+
+def test_golden_fixture_inputs_follow_generators(golden_solves):
+    from paper_2503_03456_b200 import problems as P
+    s = golden_solves
+    p = P.make("c0", 24, 20, seed=1)
+    assert np.array_equal(s["c0_24x20_A"], p.A) and np.array_equal(s["c0_24x20_C"], p.C)
