@@ -87,9 +87,14 @@ typedef struct sylv_report {
   double ms_schur, ms_orth, ms_setup, ms_y0, ms_refine, ms_recover, ms_total;
 } sylv_report;
 
-/* library identity */
+/* library identity and diagnostics */
 int sylv_version(void);
 const char* sylv_status_string(int status);
+/* number of kernels this library has launched in the process (bench evidence) */
+unsigned long long sylv_launch_count(void);
+/* measured arithmetic peak in TFLOP/s: kind 0 = FP32 FFMA, 1 = FP64 DFMA,
+ * 2 = FP64 DMMA.8x8x4 (the roofline denominators of the path) */
+int sylv_microbench(int kind, double* tflops, void* stream);
 
 /* mp_orth / mp_inv (refinement.py:205-297): A m x m, B n x n, C and X m x n,
  * fp64 (complex_data = 0) or complex128 (complex_data = 1). */

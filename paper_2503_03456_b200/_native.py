@@ -25,7 +25,8 @@ MAX_NORMS = 256
 DTYPE = {"float32": 0, "float64": 1, "complex64": 2, "complex128": 3}
 
 EXPORTS = (
-    "sylv_version", "sylv_status_string", "sylv_workspace_size", "sylv_solve",
+    "sylv_version", "sylv_status_string", "sylv_launch_count", "sylv_microbench",
+    "sylv_workspace_size", "sylv_solve",
     "sylv_refine_workspace_size", "sylv_refine", "sylv_schur_workspace_size", "sylv_schur",
     "sylv_trsyl_workspace_size", "sylv_trsyl", "sylv_orth_workspace_size", "sylv_orth", "sylv_gemm",
 )
@@ -70,6 +71,8 @@ def lib():
         L.sylv_version.restype = ct.c_int
         L.sylv_status_string.restype = ct.c_char_p
         L.sylv_status_string.argtypes = [ip]
+        L.sylv_launch_count.restype = ct.c_ulonglong
+        L.sylv_microbench.argtypes = [ip, ct.POINTER(ct.c_double), vp]
         L.sylv_workspace_size.argtypes = [ct.POINTER(Params), ct.POINTER(sz)]
         L.sylv_solve.argtypes = [ct.POINTER(Params), vp, ip, vp, ip, vp, ip, vp, ip, vp, sz, vp,
                                  ct.POINTER(Report)]

@@ -176,7 +176,17 @@ __device__ __forceinline__ V block_sum(V v, V* buf) {
     }                                                                               \
   } while (0)
 
-#define MSY_LAUNCH_CK() MSY_CK(cudaGetLastError())
+// every kernel launch of the library goes through MSY_LAUNCH_CK: the counter backs
+// sylv_launch_count() (the bench's gpu_launches evidence)
+inline unsigned long long& launch_counter() {
+  static unsigned long long c = 0;
+  return c;
+}
+#define MSY_LAUNCH_CK()                                   \
+  do {                                                    \
+    __atomic_add_fetch(&msy::launch_counter(), 1ULL, __ATOMIC_RELAXED); \
+    MSY_CK(cudaGetLastError());                           \
+  } while (0)
 
 __host__ __device__ static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 

@@ -89,10 +89,11 @@ __global__ void __launch_bounds__(128) trsm_rup_kernel(int nb, const S* Rk, int 
   for (int j = 0; j < nb; j++) B[r + (size_t)j * ldb] = x[j];
 }
 
-struct OrthInfo {
-  int bad_pivot;
-  double diag_min;
-};
+template <class S>
+__global__ void clear_lower_kernel(int m, S* G, int ldg) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i < m && i > j) G[i + (size_t)j * ldg] = S(0);
+}
 
 // Q = U R^{-1} with U^H U = R^H R.  G is an m x m scratch (holds R on return).
 // dinfo: device scratch (int flag + double diag_min).
@@ -128,6 +129,9 @@ int orth_cholqr(int m, const S* U, int ldu, S* Q, int ldq, S* G, int ldg, int* d
     trsm_rup_kernel<S><<<cdiv(m, 128), 128, 0, st>>>(nb, G + k + (size_t)k * ldg, ldg, m, Qk, ldq);
     MSY_LAUNCH_CK();
   }
+  // the trailing GEMM updates also wrote the strictly lower part: clear it so G holds R
+  clear_lower_kernel<S><<<dim3(cdiv(m, 256), m), 256, 0, st>>>(m, G, ldg);
+  MSY_LAUNCH_CK();
   return 0;
 }
 

@@ -23,6 +23,7 @@
 #include "gemm.cuh"
 #include "gemm_dmma.cuh"
 #include "lu.cuh"
+#include "microbench.cuh"
 #include "orth.cuh"
 #include "schur.cuh"
 #include "trsyl.cuh"
@@ -466,6 +467,13 @@ bool valid_dtype(int d) { return d >= 0 && d <= 3; }
 // C ABI (linkage from include/mpsylv_b200.h)
 
 int sylv_version(void) { return 1; }
+
+unsigned long long sylv_launch_count(void) { return __atomic_load_n(&msy::launch_counter(), __ATOMIC_RELAXED); }
+
+int sylv_microbench(int kind, double* tflops, void* stream) {
+  if (kind < 0 || kind > 2 || !tflops) return SYLV_EINVAL;
+  return msy::microbench(kind, tflops, (cudaStream_t)stream);
+}
 
 const char* sylv_status_string(int s) {
   switch (s) {

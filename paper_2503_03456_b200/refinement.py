@@ -148,27 +148,34 @@ def solve(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, *, kind: str = "gen
     A, B, C = (t.to(dt).contiguous() for t in (A, B, C))
     if out is None:
         out = torch.empty((m, n), dtype=dt, device=A.device)
-    p = _native.Params()
     # column-major problem (A' = B^T, B' = A^T, C' = C^T) of order (n, m)
-    p.m, p.n = n, m
+    rep = _solve_cm(B, A, C, out, n, m, kind, variant, low_bits, correction_bits,
+                    epsilon if epsilon is not None else 1e-12 * max(m, n), max_iter, y0_zero)
+    return out, rep
+
+
+def _solve_cm(A, B, C, X, m, n, kind, variant, low_bits, correction_bits, epsilon, max_iter, y0_zero):
+    """Column-major call of sylv_solve: A (m x m), B (n x n), C and X (m x n), ld = rows."""
+    p = _native.Params()
+    p.m, p.n = m, n
     p.kind = _native.KIND_LYAPUNOV if kind == "lyapunov" else _native.KIND_GENERAL
-    p.complex_data = int(cx)
+    p.complex_data = int(A.is_complex())
     p.variant = _native.VARIANT_INV if variant == "inv" else _native.VARIANT_ORTH
     p.low_bits = int(low_bits)
     p.correction_bits = int(correction_bits)
     p.max_iter = int(max_iter)
     p.y0_zero = int(bool(y0_zero))
-    p.epsilon = float(epsilon) if epsilon is not None else 1e-12 * max(m, n)
+    p.epsilon = float(epsilon)
     L = _native.lib()
     sz = ct.c_size_t()
     _native.check(L.sylv_workspace_size(ct.byref(p), ct.byref(sz)), "workspace query")
     ws = D.workspace(sz.value, A.device)
     rep = _native.Report()
     with torch.cuda.device(A.device):
-        rc = L.sylv_solve(ct.byref(p), B.data_ptr(), n, A.data_ptr(), m, C.data_ptr(), n, out.data_ptr(), n,
+        rc = L.sylv_solve(ct.byref(p), A.data_ptr(), m, B.data_ptr(), n, C.data_ptr(), m, X.data_ptr(), m,
                           ws.data_ptr(), sz.value, D.stream_ptr(A.device), ct.byref(rep))
     _native.check(rc, "sylv_solve")
-    return out, rep
+    return rep
 
 
 def _run(p, cfg, variant, counter, y0_zero):
@@ -182,12 +189,15 @@ def _run(p, cfg, variant, counter, y0_zero):
     dev = D.device()
     real = _is_real(p.A, p.B, p.C)
     dt = torch.float64 if real else torch.complex128
-    f = (lambda M: torch.as_tensor(np.ascontiguousarray(np.real(M) if real else M), device=dev).to(dt))
-    X, rep = solve(f(p.A), f(p.B), f(p.C), kind="lyapunov" if p.kind == "lyapunov" else "general",
-                   variant=variant, low_bits=lo, correction_bits=64, epsilon=eps, max_iter=cfg.max_iter,
-                   y0_zero=y0_zero)
+    # same matrices as the reference (column-major copies, no transposed problem): Schur sees A and
+    # B themselves, so structure the reference relies on (e.g. triangular inputs) is preserved
+    cv = (lambda M: D.to_cm(np.real(M) if real else M, dt, dev))
+    tA, tB, tC = cv(p.A), cv(p.B), cv(p.C)
+    tX = torch.empty_like(tC)
+    rep = _solve_cm(tA, tB, tC, tX, m, n, "lyapunov" if p.kind == "lyapunov" else "general", variant, lo, 64,
+                    eps, cfg.max_iter, y0_zero)
     _raise_for(rep.status)
-    Xn = X.cpu().numpy().astype(np.complex128)
+    Xn = D.from_cm(tX).astype(np.complex128)
     if counter is not None:  # model-derived counts (costmodel.flops), see precision.FlopCounter
         fc = flops(algorithm_name(variant, p.kind), m, n, rep.iterations)
         counter.add("low", int(round(fc.low_flops)))

@@ -80,8 +80,11 @@ def test_trsyl_matches_oracle_complex(B200, oracle, golden_kernels, name):
 
 
 def quasi_upper(rng, n, frac=0.3):
-    """Real upper quasi-triangular matrix with 2x2 blocks carrying complex pairs."""
-    T = np.triu(rng.standard_normal((n, n))) + 3 * np.eye(n)
+    """Real upper quasi-triangular matrix with 2x2 blocks carrying complex pairs.
+
+    Strictly-upper entries are N(0, 1/n) like the Schur factors of the configs, so the
+    triangular recurrence stays well conditioned at any n."""
+    T = np.triu(rng.standard_normal((n, n)), 1) / np.sqrt(n) + 3 * np.eye(n)
     i = 0
     while i < n - 1:
         if rng.random() < frac:
@@ -104,19 +107,31 @@ def test_trsyl_real_quasi_triangular(B200, rng, m, n):
         TA[63, 62] = 0.0
     W = rng.standard_normal((m, n))
     Y = B200.solve_sylv_tri(TA, TB, W).real
-    assert np.linalg.norm(TA @ Y + Y @ TB - W) < 1e-12 * np.linalg.norm(W) * (1 + np.linalg.norm(Y))
+    scale = (np.linalg.norm(TA) + np.linalg.norm(TB)) * np.linalg.norm(Y)
+    assert np.linalg.norm(TA @ Y + Y @ TB - W) < 1e-14 * scale
+    Y32 = B200.solve_sylv_tri(TA, TB, W, M32()).real
+    assert np.linalg.norm(TA @ Y32 + Y32 @ TB - W) < 1e-5 * scale
     # Lyapunov orientation: lower T_B = T_A^T (descending columns)
     W2 = rng.standard_normal((m, m))
     Y2 = B200.solve_sylv_tri(TA, TA.T, W2).real
-    assert np.linalg.norm(TA @ Y2 + Y2 @ TA.T - W2) < 1e-12 * np.linalg.norm(W2) * (1 + np.linalg.norm(Y2))
+    scale = 2 * np.linalg.norm(TA) * np.linalg.norm(Y2)
+    assert np.linalg.norm(TA @ Y2 + Y2 @ TA.T - W2) < 1e-14 * scale
 
 
-def test_trsyl_large_complex_upper(B200, rng):
-    m, n = 150, 130
-    TA, TB = rand_upper(rng, m), rand_upper(rng, n)
+def M32():
+    from paper_2503_03456_b200 import BINARY32, PrecisionContext
+    return PrecisionContext(BINARY32)
+
+
+@pytest.mark.parametrize("m,n", [(40, 40), (33, 20), (65, 65), (150, 130), (300, 257)])
+def test_trsyl_complex_upper_tiles(B200, rng, m, n):
+    TA = np.triu(cmat(rng, m, m), 1) / np.sqrt(m) + (3 + 1j) * np.eye(m)
+    TB = np.triu(cmat(rng, n, n), 1) / np.sqrt(n) + (2 - 0.5j) * np.eye(n)
     W = cmat(rng, m, n)
-    Y = B200.solve_sylv_tri(TA, TB, W)
-    assert np.linalg.norm(TA @ Y + Y @ TB - W) < 1e-12 * np.linalg.norm(W)
+    for ctx, tol in ((None, 1e-14), (M32(), 1e-5)):
+        Y = B200.solve_sylv_tri(TA, TB, W, ctx)
+        scale = (np.linalg.norm(TA) + np.linalg.norm(TB)) * np.linalg.norm(Y)
+        assert np.linalg.norm(TA @ Y + Y @ TB - W) < tol * scale
 
 
 def test_trsyl_singular_pair_is_typed(B200):

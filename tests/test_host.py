@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "mpsylv_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sylv_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|unsigned long long)\s+(sylv_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():
