@@ -17,8 +17,41 @@
 namespace msy {
 
 constexpr int HESS_NB = 32;     // panel width
-constexpr int HESS_CHUNK = 256;  // gemv column chunk
-constexpr int HESS_TPB = 1024;
+constexpr int HESS_CHUNK = 64;  // gemv column chunk
+constexpr int HESS_ROWS = 128;  // gemv rows per CTA
+constexpr int HESS_TPB = 512;
+
+// out[q] = sum_r conj(V[r, q]) x[r] over rows r0..m-1 for q < nq (nq <= HESS_NB):
+// every thread accumulates all nq partial sums over its rows (independent loads),
+// then one warp-shuffle tree per q and a cross-warp pass through shared memory.
+template <class S>
+__device__ __forceinline__ void batched_vhx(int m, int r0, const S* V, int ldv, int nq, const S* x, S* out,
+                                            S (*redS)[HESS_TPB / 32]) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  S acc[HESS_NB];
+#pragma unroll
+  for (int q = 0; q < HESS_NB; q++) acc[q] = S(0);
+  for (int r = r0 + tid; r < m; r += nt) {
+    const S xv = x[r];
+#pragma unroll
+    for (int q = 0; q < HESS_NB; q++)
+      if (q < nq) acc[q] = fmacc(V[r + (size_t)q * ldv], xv, acc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < HESS_NB; q++) {
+    if (q < nq) {
+      S s = warp_sum(acc[q]);
+      if (lane == 0) redS[q][wid] = s;
+    }
+  }
+  __syncthreads();
+  if (tid < nq) {
+    S s = S(0);
+    for (int w = 0; w < nw; w++) s += redS[tid][w];
+    out[tid] = s;
+  }
+  __syncthreads();
+}
 
 // V: m x m buffer (column c = reflector of column c, zero above row c+1)
 // Y: m x NB, T: NB x NB (this panel), part: nch x m partial gemv sums,
@@ -30,32 +63,20 @@ __global__ void __launch_bounds__(HESS_TPB) hess_col_kernel(int m, S* A, int lda
   typedef typename tr<S>::R R;
   __shared__ S u[HESS_NB];
   __shared__ S w[HESS_NB];
+  __shared__ S vrow[HESS_NB];
   __shared__ S redS[HESS_NB][HESS_TPB / 32];
   __shared__ R redR[HESS_TPB / 32];
   __shared__ S sh_beta, sh_tau, sh_scal;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   const int c = k + i;
+  const S* Vp = V + (size_t)k * ldv;  // this panel's reflectors
 
   // ---- finish Y[:, i-1] and T[:, i-1] ----
   if (i > 0) {
     const int j = i - 1, cj = k + j;
     const S* vj = V + (size_t)cj * ldv;
-    // u[q] = V[:, q]^H v_j, q < j (rows cj+1..m-1 are the only nonzeros of v_j)
-    for (int q = 0; q < j; q++) {
-      const S* vq = V + (size_t)(k + q) * ldv;
-      S s = S(0);
-      for (int r = cj + 1 + tid; r < m; r += nt) s = fmacc(vq[r], vj[r], s);
-      s = warp_sum(s);
-      if (lane == 0) redS[q][wid] = s;
-    }
-    __syncthreads();
-    if (tid < j) {
-      S s = S(0);
-      for (int q = 0; q < nw; q++) s += redS[tid][q];
-      u[tid] = s;
-    }
-    __syncthreads();
-    S tj = tau[cj];
+    batched_vhx<S>(m, cj + 1, Vp, ldv, j, vj, u, redS);  // u = V[:, 0:j]^H v_j
+    const S tj = tau[cj];
     for (int r = tid; r < m; r += nt) {
       S y = S(0);
       for (int ch = 0; ch < nch; ch++) y += part[(size_t)ch * m + r];
@@ -73,29 +94,18 @@ __global__ void __launch_bounds__(HESS_TPB) hess_col_kernel(int m, S* A, int lda
   if (i >= nbp) return;
 
   S* ac = A + (size_t)c * lda;
-  // ---- right ops of reflectors 0..i-1 on column c (all rows) ----
   if (i > 0) {
+    // ---- right ops of reflectors 0..i-1 on column c (all rows): a -= Y V[c, 0:i]^H ----
+    if (tid < i) vrow[tid] = conj(Vp[c + (size_t)tid * ldv]);
+    __syncthreads();
     for (int r = tid; r < m; r += nt) {
       S a = ac[r];
-      for (int q = 0; q < i; q++) a = a - Y[r + (size_t)q * ldy] * conj(V[c + (size_t)(k + q) * ldv]);
+      for (int q = 0; q < i; q++) a = a - Y[r + (size_t)q * ldy] * vrow[q];
       ac[r] = a;
     }
     __syncthreads();
     // ---- left ops: a[k+1:m] -= V T^H (V^H a) ----
-    for (int q = 0; q < i; q++) {
-      const S* vq = V + (size_t)(k + q) * ldv;
-      S s = S(0);
-      for (int r = k + q + 1 + tid; r < m; r += nt) s = fmacc(vq[r], ac[r], s);
-      s = warp_sum(s);
-      if (lane == 0) redS[q][wid] = s;
-    }
-    __syncthreads();
-    if (tid < i) {
-      S s = S(0);
-      for (int q = 0; q < nw; q++) s += redS[tid][q];
-      u[tid] = s;
-    }
-    __syncthreads();
+    batched_vhx<S>(m, k + 1, Vp, ldv, i, ac, u, redS);
     if (tid < i) {  // w = T^H u  (T upper => T^H lower)
       S s = S(0);
       for (int q = 0; q <= tid; q++) s = fmacc(T[q + tid * ldt], u[q], s);
@@ -104,7 +114,7 @@ __global__ void __launch_bounds__(HESS_TPB) hess_col_kernel(int m, S* A, int lda
     __syncthreads();
     for (int r = k + 1 + tid; r < m; r += nt) {
       S a = ac[r];
-      for (int q = 0; q < i; q++) a = a - V[r + (size_t)(k + q) * ldv] * w[q];
+      for (int q = 0; q < i; q++) a = a - Vp[r + (size_t)q * ldv] * w[q];
       ac[r] = a;
     }
     __syncthreads();
@@ -141,27 +151,27 @@ __global__ void __launch_bounds__(HESS_TPB) hess_col_kernel(int m, S* A, int lda
   }
 }
 
-// part[ch][r] = sum over columns q in chunk ch (q > c) of A[r, q] v[q]
+// part[ch][r] = sum over columns q in chunk ch (q >= c0) of A[r, q] v[q]
 template <class S>
-__global__ void __launch_bounds__(256) hess_gemv_kernel(int m, const S* __restrict__ A, int lda, int c0,
-                                                        const S* __restrict__ v, S* part) {
-  const int r = blockIdx.x * 256 + threadIdx.x;
+__global__ void __launch_bounds__(HESS_ROWS) hess_gemv_kernel(int m, const S* __restrict__ A, int lda, int c0,
+                                                              const S* __restrict__ v, S* part) {
+  const int r = blockIdx.x * HESS_ROWS + threadIdx.x;
   const int ch = blockIdx.y;
   const int q0 = c0 + ch * HESS_CHUNK, q1 = min(m, q0 + HESS_CHUNK);
   __shared__ S vs[HESS_CHUNK];
-  for (int q = q0 + threadIdx.x; q < q1; q += 256) vs[q - q0] = v[q];
+  for (int q = q0 + threadIdx.x; q < q1; q += HESS_ROWS) vs[q - q0] = v[q];
   __syncthreads();
   if (r >= m) return;
-  S s0 = S(0), s1 = S(0), s2 = S(0), s3 = S(0);
+  S s[8];
+#pragma unroll
+  for (int u = 0; u < 8; u++) s[u] = S(0);
   int q = q0;
-  for (; q + 3 < q1; q += 4) {
-    s0 = fmac(A[r + (size_t)q * lda], vs[q - q0], s0);
-    s1 = fmac(A[r + (size_t)(q + 1) * lda], vs[q + 1 - q0], s1);
-    s2 = fmac(A[r + (size_t)(q + 2) * lda], vs[q + 2 - q0], s2);
-    s3 = fmac(A[r + (size_t)(q + 3) * lda], vs[q + 3 - q0], s3);
+  for (; q + 7 < q1; q += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) s[u] = fmac(A[r + (size_t)(q + u) * lda], vs[q + u - q0], s[u]);
   }
-  for (; q < q1; q++) s0 = fmac(A[r + (size_t)q * lda], vs[q - q0], s0);
-  part[(size_t)ch * m + r] = (s0 + s1) + (s2 + s3);
+  for (; q < q1; q++) s[0] = fmac(A[r + (size_t)q * lda], vs[q - q0], s[0]);
+  part[(size_t)ch * m + r] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
 template <class S>
@@ -213,7 +223,7 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
       MSY_LAUNCH_CK();
       // gemv with v_i over columns c+1..m-1
       int nchn = cdiv(m - (c + 1), HESS_CHUNK);
-      hess_gemv_kernel<S><<<dim3(cdiv(m, 256), nchn), 256, 0, st>>>(m, A, lda, c + 1, w.V + (size_t)c * ldv, w.part);
+      hess_gemv_kernel<S><<<dim3(cdiv(m, HESS_ROWS), nchn), HESS_ROWS, 0, st>>>(m, A, lda, c + 1, w.V + (size_t)c * ldv, w.part);
       MSY_LAUNCH_CK();
     }
     {  // finish Y[:, nbp-1]

@@ -20,18 +20,51 @@
 namespace msy {
 
 template <class S> struct MsCfg;
-template <> struct MsCfg<float> { static constexpr int W = 128, NB = 16; };
-template <> struct MsCfg<double> { static constexpr int W = 96, NB = 12; };
-template <> struct MsCfg<cfloat> { static constexpr int W = 96, NB = 12; };
-template <> struct MsCfg<cdouble> { static constexpr int W = 64, NB = 8; };
+template <> struct MsCfg<float> { static constexpr int W = 160, NB = 24; };
+template <> struct MsCfg<double> { static constexpr int W = 112, NB = 16; };
+template <> struct MsCfg<cfloat> { static constexpr int W = 112, NB = 16; };
+template <> struct MsCfg<cdouble> { static constexpr int W = 80, NB = 10; };
+constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
+
+// correctly rounded reciprocal (cheaper than a full division on the critical path)
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+template <class R> __device__ __forceinline__ cplx<R> rcp_rn(cplx<R> x) {
+  R d = rcp_rn(x.x * x.x + x.y * x.y);
+  return cplx<R>(x.x * d, -x.y * d);
+}
+
+// Householder reflector for a 2/3-vector, every lane computing it redundantly
+template <class S>
+__device__ __forceinline__ void refl3_fast(int nr, S x0, S x1, S x2, S& beta, S& tau, S& v1, S& v2) {
+  typedef typename tr<S>::R R;
+  R xn2 = abs2(x1) + (nr > 2 ? abs2(x2) : R(0));
+  if (xn2 == R(0) && im(x0) == R(0)) {
+    tau = S(0); beta = x0; v1 = S(0); v2 = S(0);
+    return;
+  }
+  R nrm = sqrt(abs2(x0) + xn2);
+  R b = re(x0) >= R(0) ? -nrm : nrm;
+  beta = mk<S>(b);
+  tau = (mk<S>(b) - x0) * mk<S>(rcp_rn(b));
+  S scal = rcp_rn(x0 - mk<S>(b));
+  v1 = x1 * scal;
+  v2 = nr > 2 ? x2 * scal : S(0);
+}
 
 // ---------------------------------------------------------------------------
-// window chase
+// window chase: one CTA, one warp per bulge, the W x W window of H and its
+// accumulated Z in shared memory.  Per step: every active bulge computes its
+// reflector (all lanes, broadcast reads), applies it from the left to the
+// window's rows (phase A), then from the right to the window's columns and
+// to Z (phase B).  Bulges sit 4 rows apart, so one step's bulges touch disjoint
+// rows/columns; the two phases order the only overlapping entries.
 template <class S>
-__global__ void __launch_bounds__(512) chase_kernel(S* H, int ldh, int lo, int hi, int nb,
-                                                    const typename tr<S>::R* __restrict__ shifts, int ws, int we,
-                                                    int t0, int t1, S* Zg) {
+__global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int hi, int nb,
+                                                     const typename tr<S>::R* __restrict__ shifts, int ws, int we,
+                                                     int t0, int t1, S* Zg) {
   typedef typename tr<S>::R R;
+  constexpr int KM = (MsCfg<S>::W + 31) / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = we - ws;
   const int ld = nw + 1;
@@ -47,38 +80,46 @@ __global__ void __launch_bounds__(512) chase_kernel(S* H, int ldh, int lo, int h
   }
   __syncthreads();
   const int j = warp;  // bulge handled by this warp
+  const int span1 = hi - lo - 1;
   for (int t = t0; t < t1; t++) {
     const int p = lo - 1 + t - 4 * j;  // global position
     const bool act = (j < nb) && (p >= lo - 1) && (p <= hi - 2);
     S tau = S(0), v1 = S(0), v2 = S(0), beta = S(0);
-    int nr = 0, pl = p - ws;  // window-local position
+    const int pl = p - ws;  // window-local position
+    const int nr = (hi - p) >= 3 ? 3 : 2;
     if (act) {
-      nr = (hi - p) >= 3 ? 3 : 2;
-      if (lane == 0) {
-        S x0, x1, x2;
-        if (p == lo - 1) {
-          const R* w4 = shifts + 4 * j;
-          int l = lo - ws;
-          shift_poly<S>(HW(l, l), HW(l + 1, l), HW(l, l + 1), HW(l + 1, l + 1), (lo + 2 <= hi) ? HW(l + 2, l + 1) : S(0),
-                        w4, x0, x1, x2);
-        } else {
-          x0 = HW(pl + 1, pl); x1 = HW(pl + 2, pl); x2 = nr > 2 ? HW(pl + 3, pl) : S(0);
-        }
-        make_refl3<S>(nr, x0, x1, x2, beta, tau, v1, v2);
+      S x0, x1, x2;
+      if (p == lo - 1) {
+        const R* w4 = shifts + 4 * j;
+        const int l = lo - ws;
+        shift_poly<S>(HW(l, l), HW(l + 1, l), HW(l, l + 1), HW(l + 1, l + 1), (lo + 2 <= hi) ? HW(l + 2, l + 1) : S(0),
+                      w4, x0, x1, x2);
+      } else {
+        x0 = HW(pl + 1, pl); x1 = HW(pl + 2, pl); x2 = nr > 2 ? HW(pl + 3, pl) : S(0);
       }
-      tau = shfl(tau, 0); v1 = shfl(v1, 0); v2 = shfl(v2, 0); beta = shfl(beta, 0);
-      // phase A: left op on rows pl+1..pl+nr, window columns (p+1 or lo)..we-1
+      refl3_fast<S>(nr, x0, x1, x2, beta, tau, v1, v2);
+      __syncwarp();
       if (!iszero(tau)) {
-        S ctau = conj(tau);
-        const int c0 = pl + 1;
-        for (int c = c0 + lane; c < nw; c += 32) {
-          S h0 = HW(pl + 1, c), h1 = HW(pl + 2, c), h2 = nr > 2 ? HW(pl + 3, c) : S(0);
-          S w = fmacc(v1, h1, h0);
-          if (nr > 2) w = fmacc(v2, h2, w);
-          w = ctau * w;
-          HW(pl + 1, c) = h0 - w;
-          HW(pl + 2, c) = h1 - v1 * w;
-          if (nr > 2) HW(pl + 3, c) = h2 - v2 * w;
+        const S ctau = conj(tau);
+        S h0[KM], h1[KM], h2[KM];
+#pragma unroll
+        for (int k = 0; k < KM; k++) {
+          const int c = pl + 1 + lane + 32 * k;
+          if (c < nw) {
+            h0[k] = HW(pl + 1, c); h1[k] = HW(pl + 2, c); h2[k] = nr > 2 ? HW(pl + 3, c) : S(0);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KM; k++) {
+          const int c = pl + 1 + lane + 32 * k;
+          if (c < nw) {
+            S w = fmacc(v1, h1[k], h0[k]);
+            if (nr > 2) w = fmacc(v2, h2[k], w);
+            w = ctau * w;
+            HW(pl + 1, c) = h0[k] - w;
+            HW(pl + 2, c) = h1[k] - v1 * w;
+            if (nr > 2) HW(pl + 3, c) = h2[k] - v2 * w;
+          }
         }
       }
       if (p >= lo && lane == 0) {
@@ -89,19 +130,37 @@ __global__ void __launch_bounds__(512) chase_kernel(S* H, int ldh, int lo, int h
     }
     __syncthreads();
     if (act && !iszero(tau)) {
-      // phase B: right op on columns pl+1..pl+nr, window rows 0..min(p+4,hi)-ws; Z all rows
+      // rows of H touched: window rows 0..min(p+4,hi); rows of Z that can be nonzero:
+      // 0..(front bulge position + 3) -- rows below were never mixed in this pass
       const int rmax = ((p + 4 < hi) ? p + 4 : hi) - ws;
-      for (int e = lane; e < nw + rmax + 1; e += 32) {
-        S* M;
-        int r;
-        if (e <= rmax) { M = Hw; r = e; } else { M = Zw; r = e - rmax - 1; }
-        S h0 = M[r + (pl + 1) * ld], h1 = M[r + (pl + 2) * ld], h2 = nr > 2 ? M[r + (pl + 3) * ld] : S(0);
-        S w = fmac(h1, v1, h0);
-        if (nr > 2) w = fmac(h2, v2, w);
-        w = tau * w;
-        M[r + (pl + 1) * ld] = h0 - w;
-        M[r + (pl + 2) * ld] = h1 - w * conj(v1);
-        if (nr > 2) M[r + (pl + 3) * ld] = h2 - w * conj(v2);
+      const int x = t - span1;
+      const int jh = x > 0 ? (x + 3) / 4 : 0;
+      const int zmax = min(nw - 1, (lo - 1 + t - 4 * jh) - ws + 3);
+#pragma unroll
+      for (int pass = 0; pass < 2; pass++) {
+        S* M = pass == 0 ? Hw : Zw;
+        const int last = pass == 0 ? rmax : zmax;
+        S a0[KM], a1[KM], a2[KM];
+#pragma unroll
+        for (int k = 0; k < KM; k++) {
+          const int r = lane + 32 * k;
+          if (r <= last) {
+            a0[k] = M[r + (pl + 1) * ld]; a1[k] = M[r + (pl + 2) * ld];
+            a2[k] = nr > 2 ? M[r + (pl + 3) * ld] : S(0);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KM; k++) {
+          const int r = lane + 32 * k;
+          if (r <= last) {
+            S w = fmac(a1[k], v1, a0[k]);
+            if (nr > 2) w = fmac(a2[k], v2, w);
+            w = tau * w;
+            M[r + (pl + 1) * ld] = a0[k] - w;
+            M[r + (pl + 2) * ld] = a1[k] - w * conj(v1);
+            if (nr > 2) M[r + (pl + 3) * ld] = a2[k] - w * conj(v2);
+          }
+        }
       }
     }
     __syncthreads();
@@ -116,24 +175,25 @@ __global__ void __launch_bounds__(512) chase_kernel(S* H, int ldh, int lo, int h
 }
 
 // ---------------------------------------------------------------------------
-// in-place application of a small orthogonal Z (nz x nz, ld nz):
+// in-place application of a small orthogonal Z (nz x nz, ld nz, nz <= ZMAX):
 //   region L: H[r0:r0+nz, cL0:cL1] <- Z^H * (.)       (tiles of 32 columns)
-//   region R: H[0:rR1, c0:c0+nz]   <- (.) * Z          (tiles of 32 rows)
-//   region U: U[0:mU, c0:c0+nz]    <- (.) * Z
+//   region R: H[0:rR1, r0:r0+nz]   <- (.) * Z          (tiles of 32 rows)
+//   region U: U[0:mU, r0:r0+nz]    <- (.) * Z
 template <class S>
 __global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restrict__ Zg, S* H, int ldh, int r0,
                                                       int cL0, int cL1, int rR1, S* U, int ldu, int mU) {
+  constexpr int ZA = ZMAX / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ldz = nz + 1;
   S* Zs = (S*)smem_raw;
-  S* Ts = Zs + (size_t)ldz * nz;  // tile: nz x 33 (L) or 32 x (nz+1) (R)
+  S* Ts = Zs + (size_t)ldz * nz;
   const int tid = threadIdx.x;
-  const int ntL = cdiv(cL1 - cL0, 32), ntR = cdiv(rR1, 32), ntU = cdiv(mU, 32);
+  const int ntL = cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0, ntR = cdiv(rR1, 32), ntU = cdiv(mU, 32);
   int b = blockIdx.x;
   for (int e = tid; e < nz * nz; e += 256) Zs[(e % nz) + (e / nz) * ldz] = Zg[e];
   if (b < ntL) {
     const int c0 = cL0 + b * 32, nc = min(32, cL1 - c0);
-    const int ldt = nz + 1;  // tile stored transposed-free: Ts[r + c*ldt]
+    const int ldt = nz + 1;  // Ts[r + c*ldt], nz rows x 32 columns
     for (int e = tid; e < nz * 32; e += 256) {
       int r = e % nz, c = e / nz;
       Ts[r + c * ldt] = c < nc ? H[(r0 + r) + (size_t)(c0 + c) * ldh] : S(0);
@@ -141,24 +201,24 @@ __global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restric
     __syncthreads();
     // out[i, c] = sum_r conj(Z[r, i]) T[r, c]; thread: rows i = tr + 32a, cols c = 4 tc + q
     const int tr_ = tid & 31, tc = tid >> 5;
-    S acc[4][4];
+    S acc[ZA][4];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
+    for (int a = 0; a < ZA; a++)
 #pragma unroll
       for (int q = 0; q < 4; q++) acc[a][q] = S(0);
     for (int r = 0; r < nz; r++) {
-      S z[4], t[4];
+      S z[ZA], t[4];
 #pragma unroll
-      for (int a = 0; a < 4; a++) { int i = tr_ + 32 * a; z[a] = i < nz ? conj(Zs[r + i * ldz]) : S(0); }
+      for (int a = 0; a < ZA; a++) { int i = tr_ + 32 * a; z[a] = i < nz ? conj(Zs[r + i * ldz]) : S(0); }
 #pragma unroll
       for (int q = 0; q < 4; q++) t[q] = Ts[r + (4 * tc + q) * ldt];
 #pragma unroll
-      for (int a = 0; a < 4; a++)
+      for (int a = 0; a < ZA; a++)
 #pragma unroll
         for (int q = 0; q < 4; q++) acc[a][q] = fmac(z[a], t[q], acc[a][q]);
     }
 #pragma unroll
-    for (int a = 0; a < 4; a++) {
+    for (int a = 0; a < ZA; a++) {
       int i = tr_ + 32 * a;
       if (i >= nz) continue;
 #pragma unroll
@@ -174,29 +234,26 @@ __global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restric
   int ldm, rbase, nrows;
   if (b < ntR) { M = H; ldm = ldh; rbase = b * 32; nrows = min(32, rR1 - rbase); }
   else { b -= ntR; if (b >= ntU) return; M = U; ldm = ldu; rbase = b * 32; nrows = min(32, mU - rbase); }
-  const int c0 = (M == H) ? (r0) : r0;  // region columns start at r0 (== window start)
-  const int ldt = nz + 1;               // Ts[r + c*32]: 32 rows x nz cols
   for (int e = tid; e < 32 * nz; e += 256) {
     int r = e % 32, c = e / 32;
-    Ts[r + c * 32] = r < nrows ? M[(rbase + r) + (size_t)(c0 + c) * ldm] : S(0);
+    Ts[r + c * 32] = r < nrows ? M[(rbase + r) + (size_t)(r0 + c) * ldm] : S(0);
   }
-  (void)ldt;
   __syncthreads();
   // out[r, j] = sum_i T[r, i] Z[i, j]; thread: rows r = 4g + q, cols j = lane + 32a
   const int lane = tid & 31, g = tid >> 5;
-  S acc[4][4];
+  S acc[ZA][4];
 #pragma unroll
-  for (int a = 0; a < 4; a++)
+  for (int a = 0; a < ZA; a++)
 #pragma unroll
     for (int q = 0; q < 4; q++) acc[a][q] = S(0);
   for (int i = 0; i < nz; i++) {
-    S z[4], t[4];
+    S z[ZA], t[4];
 #pragma unroll
-    for (int a = 0; a < 4; a++) { int jj = lane + 32 * a; z[a] = jj < nz ? Zs[i + jj * ldz] : S(0); }
+    for (int a = 0; a < ZA; a++) { int jj = lane + 32 * a; z[a] = jj < nz ? Zs[i + jj * ldz] : S(0); }
 #pragma unroll
     for (int q = 0; q < 4; q++) t[q] = Ts[(4 * g + q) + i * 32];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
+    for (int a = 0; a < ZA; a++)
 #pragma unroll
       for (int q = 0; q < 4; q++) acc[a][q] = fmac(t[q], z[a], acc[a][q]);
   }
@@ -205,9 +262,9 @@ __global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restric
     int r = 4 * g + q;
     if (r >= nrows) continue;
 #pragma unroll
-    for (int a = 0; a < 4; a++) {
+    for (int a = 0; a < ZA; a++) {
       int jj = lane + 32 * a;
-      if (jj < nz) M[(rbase + r) + (size_t)(c0 + jj) * ldm] = acc[a][q];
+      if (jj < nz) M[(rbase + r) + (size_t)(r0 + jj) * ldm] = acc[a][q];
     }
   }
 }
@@ -217,22 +274,29 @@ static size_t applyz_smem(int nz) {
   return ((size_t)(nz + 1) * nz + (size_t)(nz + 1) * 33 + 32 * (size_t)nz) * sizeof(S) + 64;
 }
 
-// Apply Z (window [w0, w0+nz)) to everything outside the window's diagonal block.
+// Apply Z (block [w0, w0+nz)) to H rows w0.. over columns [cL0, cL1), to H rows [0, rR1)
+// of the block's columns, and (if U) to all rows of U's block columns.
 template <class S>
-int apply_z(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int w0, cudaStream_t st) {
+int apply_z_regions(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int w0, int cL0, int cL1, int rR1,
+                    cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     MSY_CK(cudaFuncSetAttribute(apply_z_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)applyz_smem<S>(128)));
+                                (int)applyz_smem<S>(ZMAX)));
     attr = true;
   }
-  if (nz > 128) return -4;
-  const int cL0 = w0 + nz, cL1 = m, rR1 = w0;
-  int nblk = cdiv(cL1 - cL0, 32) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
+  if (nz > ZMAX) return -4;
+  int nblk = (cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
   if (nblk == 0) return 0;
   apply_z_kernel<S><<<nblk, 256, applyz_smem<S>(nz), st>>>(nz, Z, H, ldh, w0, cL0, cL1, rR1, U, ldu, U ? m : 0);
   MSY_LAUNCH_CK();
   return 0;
+}
+
+// Apply Z (window [w0, w0+nz)) to everything outside the window's diagonal block.
+template <class S>
+int apply_z(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int w0, cudaStream_t st) {
+  return apply_z_regions<S>(m, nz, Z, H, ldh, U, ldu, w0, w0 + nz, m, w0, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -18,7 +18,7 @@ template <class S>
 struct SchurWs {
   typedef typename tr<S>::R R;
   HessWs<S> hw;
-  S* Z;       // 128 x 128
+  S* Z;       // 2 x ZMAX^2: window factors, double-buffered across overlapping windows
   S* sblk;    // trailing block copy
   R* wr;
   R* wi;
@@ -26,7 +26,7 @@ struct SchurWs {
   int* dinfo; // small device ints
   static void carve(Arena& ar, int m, SchurWs& w) {
     if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
-    w.Z = ar.get<S>(128 * 128);
+    w.Z = ar.get<S>(2 * ZMAX * ZMAX);
     w.sblk = ar.get<S>(128 * 128);
     w.wr = ar.get<R>(256);
     w.wi = ar.get<R>(256);
@@ -39,6 +39,31 @@ struct SchurStats {
   int status, sweeps, small_calls, windows;
 };
 
+// per-host-thread auxiliary stream + events used to overlap the window chases
+// (one CTA) with the off-window Z applications (many CTAs)
+struct SweepCtx {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t evC = nullptr, evN = nullptr, evD = nullptr;
+  int dev = -1;
+};
+inline SweepCtx* sweep_ctx() {
+  thread_local SweepCtx c;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (c.aux == nullptr || c.dev != dev) {
+    cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&c.evC, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c.evN, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c.evD, cudaEventDisableTiming);
+    c.dev = dev;
+  }
+  return &c;
+}
+
+// One multishift sweep over the active block [lo, hi] with nb bulges.
+// Windows are planned on the host (bulge positions are a function of the step).
+// Pipeline: chase(k+1) on `st` runs concurrently with the far part of apply(k)
+// on `aux`; the near part (columns the next window will load) runs first.
 template <class S>
 int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const typename tr<S>::R* shifts, S* Zbuf,
              cudaStream_t st, int* nwin) {
@@ -49,6 +74,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
     MSY_CK(cudaFuncSetAttribute(chase_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
     attr = true;
   }
+  SweepCtx* sc = sweep_ctx();
   const int span = hi - lo;
   const long Tn = 4L * (nb - 1) + span;
   auto Lf = [&](long t) {
@@ -62,22 +88,50 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
     long P = lo - 1 + t - 4 * jh;
     return (int)std::min<long>(P + 4, hi);
   };
-  long t = 0;
-  while (t < Tn) {
+  struct Win { int ws, we, t0, t1; };
+  Win wins[4096];
+  int nwins = 0;
+  for (long t = 0; t < Tn;) {
     int ws = Lf(t);
     int we = std::min(ws + W, hi + 1);
     long t1 = t;
     while (t1 < Tn && Uf(t1) <= we - 1) t1++;
-    if (t1 == t) return -5;
-    int nw = we - ws;
-    chase_kernel<S><<<1, 32 * std::max(nb, 4), (size_t)2 * (nw + 1) * nw * sizeof(S), st>>>(H, ldh, lo, hi, nb, shifts,
-                                                                                         ws, we, (int)t, (int)t1, Zbuf);
-    MSY_LAUNCH_CK();
-    int rc = apply_z<S>(m, nw, Zbuf, H, ldh, U, ldu, ws, st);
-    if (rc) return rc;
-    if (nwin) (*nwin)++;
+    if (t1 == t || nwins >= 4096) return -5;
+    wins[nwins++] = {ws, we, (int)t, (int)t1};
     t = t1;
   }
+  const int nthr = 32 * std::max(nb, 4);
+  auto chase = [&](int k) -> int {
+    const Win& w = wins[k];
+    int nw = w.we - w.ws;
+    chase_kernel<S><<<1, nthr, (size_t)2 * (nw + 1) * nw * sizeof(S), st>>>(H, ldh, lo, hi, nb, shifts, w.ws, w.we,
+                                                                            w.t0, w.t1, Zbuf + (k & 1) * ZMAX * ZMAX);
+    MSY_LAUNCH_CK();
+    MSY_CK(cudaEventRecord(sc->evC, st));
+    return 0;
+  };
+  int rc = chase(0);
+  if (rc) return rc;
+  for (int k = 0; k < nwins; k++) {
+    const Win& w = wins[k];
+    const int nw = w.we - w.ws;
+    const S* Zk = Zbuf + (k & 1) * ZMAX * ZMAX;
+    const int cn = std::min(w.we + W, m);
+    MSY_CK(cudaStreamWaitEvent(sc->aux, sc->evC, 0));
+    rc = apply_z_regions<S>(m, nw, Zk, H, ldh, nullptr, ldu, w.ws, w.we, cn, 0, sc->aux);  // near
+    if (rc) return rc;
+    MSY_CK(cudaEventRecord(sc->evN, sc->aux));
+    rc = apply_z_regions<S>(m, nw, Zk, H, ldh, U, ldu, w.ws, cn, m, w.ws, sc->aux);        // far
+    if (rc) return rc;
+    if (k + 1 < nwins) {
+      MSY_CK(cudaStreamWaitEvent(st, sc->evN, 0));
+      rc = chase(k + 1);
+      if (rc) return rc;
+    }
+    if (nwin) (*nwin)++;
+  }
+  MSY_CK(cudaEventRecord(sc->evD, sc->aux));
+  MSY_CK(cudaStreamWaitEvent(st, sc->evD, 0));
   return 0;
 }
 
