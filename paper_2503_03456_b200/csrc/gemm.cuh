@@ -26,9 +26,12 @@ __device__ __forceinline__ S opval(S v) {
 }
 
 // op(A) is M x K.  OPA == 'N': A is M x K col-major; else A is K x M.
+// Split-K: blockIdx.z handles K-range [z*kchunk, (z+1)*kchunk); with `part` != null the
+// unscaled partial product goes to part + z*M*N (ld M) instead of C.
 template <class S, char OPA, char OPB>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, S alpha, const S* __restrict__ A, int lda,
-                                                        const S* __restrict__ B, int ldb, S beta, S* C, int ldc) {
+                                                        const S* __restrict__ B, int ldb, S beta, S* C, int ldc,
+                                                        int kchunk, S* part) {
   typedef GemmCfg<S> G;
   constexpr int BM = G::BM, BN = G::BN, BK = G::BK, TM = G::TM, TN = G::TN;
   constexpr int NT = (BM / TM) * (BN / TN);
@@ -44,6 +47,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, S a
 #pragma unroll
     for (int j = 0; j < TN; j++) acc[i][j] = S(0);
   S ra[LA], rb[LB];
+  const int kbeg = blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
 
   auto loadA = [&](int k0) {
 #pragma unroll
@@ -53,7 +57,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, S a
       if (OPA == 'N') { i = idx % BM; k = idx / BM; } else { k = idx % BK; i = idx / BK; }
       int gi = bm + i, gk = k0 + k;
       S v = S(0);
-      if (gi < M && gk < K) v = (OPA == 'N') ? A[gi + (size_t)gk * lda] : opval<S, OPA>(A[gk + (size_t)gi * lda]);
+      if (gi < M && gk < kend) v = (OPA == 'N') ? A[gi + (size_t)gk * lda] : opval<S, OPA>(A[gk + (size_t)gi * lda]);
       ra[e] = v;
     }
   };
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, S a
       if (OPB == 'N') { k = idx % BK; j = idx / BK; } else { j = idx % BN; k = idx / BN; }
       int gj = bn + j, gk = k0 + k;
       S v = S(0);
-      if (gj < N && gk < K) v = (OPB == 'N') ? B[gk + (size_t)gj * ldb] : opval<S, OPB>(B[gj + (size_t)gk * ldb]);
+      if (gj < N && gk < kend) v = (OPB == 'N') ? B[gk + (size_t)gj * ldb] : opval<S, OPB>(B[gj + (size_t)gk * ldb]);
       rb[e] = v;
     }
   };
@@ -86,18 +90,18 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, S a
     }
   };
 
-  int nk = (K + BK - 1) / BK;
+  int nk = (kend - kbeg + BK - 1) / BK;
   if (nk > 0) {
-    loadA(0);
-    loadB(0);
+    loadA(kbeg);
+    loadB(kbeg);
     storeAB(0);
   }
   __syncthreads();
   for (int t = 0; t < nk; t++) {
     int cur = t & 1;
     if (t + 1 < nk) {
-      loadA((t + 1) * BK);
-      loadB((t + 1) * BK);
+      loadA(kbeg + (t + 1) * BK);
+      loadB(kbeg + (t + 1) * BK);
     }
 #pragma unroll
     for (int k = 0; k < BK; k++) {
@@ -123,6 +127,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, S a
     for (int j = 0; j < TN; j++) {
       int gj = bn + ty + j * (BN / TN);
       if (gj >= N) continue;
+      if (part) {
+        part[(size_t)blockIdx.z * M * N + gi + (size_t)gj * M] = acc[i][j];
+        continue;
+      }
       S* c = &C[gi + (size_t)gj * ldc];
       S v = alpha * acc[i][j];
       if (!b0) v = fmac(beta, *c, v);
@@ -138,9 +146,53 @@ static int gemm_simt_launch(int M, int N, int K, S alpha, const S* A, int lda, c
                             int ldc, cudaStream_t st) {
   typedef GemmCfg<S> G;
   dim3 grid(cdiv(M, G::BM), cdiv(N, G::BN));
-  gemm_simt_kernel<S, OPA, OPB><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  gemm_simt_kernel<S, OPA, OPB><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, K, nullptr);
   MSY_LAUNCH_CK();
   return 0;
+}
+
+// C = alpha * sum_z part[z] + beta * C (fixed order: deterministic)
+template <class S>
+__global__ void splitk_reduce_kernel(int M, int N, int splits, const S* part, S alpha, S beta, S* C, int ldc) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i >= M) return;
+  S s = S(0);
+  for (int z = 0; z < splits; z++) s += part[(size_t)z * M * N + i + (size_t)j * M];
+  S* c = &C[i + (size_t)j * ldc];
+  S v = alpha * s;
+  if (!iszero(beta)) v = fmac(beta, *c, v);
+  *c = v;
+}
+
+template <class S, char OPA, char OPB>
+static int gemm_splitk_launch(int M, int N, int K, S alpha, const S* A, int lda, const S* B, int ldb, S beta, S* C,
+                              int ldc, S* ws, int splits, cudaStream_t st) {
+  typedef GemmCfg<S> G;
+  const int kchunk = cdiv(cdiv(K, splits), G::BK) * G::BK;
+  splits = cdiv(K, kchunk);
+  dim3 grid(cdiv(M, G::BM), cdiv(N, G::BN), splits);
+  gemm_simt_kernel<S, OPA, OPB><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ws);
+  MSY_LAUNCH_CK();
+  splitk_reduce_kernel<S><<<dim3(cdiv(M, 128), N), 128, 0, st>>>(M, N, splits, ws, alpha, beta, C, ldc);
+  MSY_LAUNCH_CK();
+  return 0;
+}
+
+// Skinny GEMMs (few output tiles, long K): split K over blockIdx.z into `ws`
+// (splits * M * N elements) and reduce in a fixed order.
+template <class S>
+int gemm_splitk(char opa, char opb, int M, int N, int K, S alpha, const S* A, int lda, const S* B, int ldb, S beta,
+                S* C, int ldc, S* ws, int splits, cudaStream_t st) {
+  if (!tr<S>::cx) {
+    if (opa == 'C') opa = 'T';
+    if (opb == 'C') opb = 'T';
+  }
+#define MSY_G(a, b) \
+  if (opa == a && opb == b) return gemm_splitk_launch<S, a, b>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, splits, st);
+  MSY_G('N', 'N') MSY_G('N', 'T') MSY_G('T', 'N') MSY_G('T', 'T')
+  if (tr<S>::cx) { MSY_G('C', 'N') MSY_G('N', 'C') MSY_G('C', 'C') MSY_G('C', 'T') MSY_G('T', 'C') }
+#undef MSY_G
+  return -2;
 }
 
 // scale C by beta (used when K == 0)

@@ -11,8 +11,15 @@
 //   per panel: trailing updates as GEMMs (right: -Y V^H; left: -V T^H V^H A).
 // Q0 is formed afterwards by backward blocked accumulation (form_q).
 #pragma once
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemm.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace msy {
 
@@ -190,9 +197,247 @@ __global__ void clear_below_sub_kernel(int m, S* A, int lda) {
   if (i < m && i > j + 1) A[i + (size_t)j * lda] = S(0);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent panel kernel: one cooperative launch per panel of HESS_NB columns.
+// Rows are split into 32-row slabs owned by the CTAs; every per-column step is
+// row-parallel, the few cross-row reductions (V^H a, ||x||, V^H v) go through a
+// deterministic two-level sum (per-CTA partials in global memory, read back by
+// every CTA in the same order), separated by grid-wide barriers.  Per column:
+//   (1) right ops of earlier panel reflectors on column c, partials of V^H a
+//   (2) left ops (a -= V T^H V^H a), partial ||a[c+2:]||^2, x0 = a[c+1]
+//   (3) reflector (computed redundantly by every CTA), v and the new column c
+//   (4) y = A[:, c+1:] v over each CTA's rows (coalesced, 8 warps split the
+//       columns), partials of V^H v
+//   (5) Y[:, i] = tau (y - Y V^H v), T[:, i]
+constexpr int HP_TPB = 512;
+constexpr int HESS_SPLITK = 16;  // K splits of the skinny V^H A products
+
+// out[q] = sum_g red[g*HESS_NB + q] for q < nq, g < G, read by the whole CTA in a fixed
+// order (8 groups of g, then the groups): deterministic, latency overlapped
+template <class S>
+__device__ __forceinline__ void cta_sum_partials(const S* red, int G, int nq, S* out, S (*scratch)[32]) {
+  constexpr int NG = HP_TPB / 32;
+  const int q = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  S s0 = S(0), s1 = S(0), s2 = S(0), s3 = S(0);
+  if (q < nq) {
+    int gg = grp;
+    for (; gg + 3 * NG < G; gg += 4 * NG) {
+      s0 += red[gg * HESS_NB + q];
+      s1 += red[(gg + NG) * HESS_NB + q];
+      s2 += red[(gg + 2 * NG) * HESS_NB + q];
+      s3 += red[(gg + 3 * NG) * HESS_NB + q];
+    }
+    for (; gg < G; gg += NG) s0 += red[gg * HESS_NB + q];
+  }
+  scratch[grp][q] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (threadIdx.x < nq) {
+    S t = S(0);
+#pragma unroll
+    for (int g8 = 0; g8 < HP_TPB / 32; g8++) t += scratch[g8][threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+constexpr int HP_ROWS = 32;
+
+template <class S>
+__global__ void __launch_bounds__(HP_TPB) hess_panel_coop_kernel(int m, S* A, int lda, int k, int nbp, S* V, int ldv,
+                                                                 S* Y, int ldy, S* T, int ldt, S* tau, S* red1,
+                                                                 S* red2, typename tr<S>::R* redR, S* slot) {
+  typedef typename tr<S>::R R;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S* sv = (S*)smem_raw;  // v (m entries)
+  __shared__ S s_vrow[HESS_NB], s_u[HESS_NB], s_w[HESS_NB];
+  __shared__ S s_part[HP_TPB / 32][HP_ROWS];
+  __shared__ S s_beta, s_tau, s_scal;
+  __shared__ R s_rsum[HP_TPB / 32];
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nslab = cdiv(m, HP_ROWS);
+  const S* Vp = V + (size_t)k * ldv;
+  for (int i = 0; i < nbp; i++) {
+    const int c = k + i;
+    S* ac = A + (size_t)c * lda;
+    // ---- (1) right ops on column c, partials of V^H a over rows >= k+1 ----
+    if (i > 0) {
+      if (tid < i) s_vrow[tid] = conj(Vp[c + (size_t)tid * ldv]);
+      __syncthreads();
+      if (warp == 0) {
+        S part[HESS_NB];
+#pragma unroll
+        for (int q = 0; q < HESS_NB; q++) part[q] = S(0);
+        for (int s = g; s < nslab; s += G) {
+          const int r = s * HP_ROWS + lane;
+          if (r < m) {
+            S a = ac[r];
+#pragma unroll
+            for (int q = 0; q < HESS_NB; q++)  // independent loads: full unroll, predicated
+              if (q < i) a = a - Y[r + (size_t)q * ldy] * s_vrow[q];
+            ac[r] = a;
+            if (r >= k + 1) {
+#pragma unroll
+              for (int q = 0; q < HESS_NB; q++)
+                if (q < i) part[q] = fmacc(Vp[r + (size_t)q * ldv], a, part[q]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < HESS_NB; q++)
+          if (q < i) {
+            S sum = warp_sum(part[q]);
+            if (lane == 0) red1[g * HESS_NB + q] = sum;
+          }
+      }
+      grid.sync();
+      // ---- (2) left ops ----
+      cta_sum_partials<S>(red1, G, i, s_u, s_part);
+      if (tid < i) {  // w = T^H u
+        S sum = S(0);
+        for (int q = 0; q <= tid; q++) sum = fmacc(T[q + tid * ldt], s_u[q], sum);
+        s_w[tid] = sum;
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      R nrm = 0;
+      for (int s = g; s < nslab; s += G) {
+        const int r = s * HP_ROWS + lane;
+        if (r < m) {
+          S a = ac[r];
+          if (i > 0 && r >= k + 1) {
+#pragma unroll
+            for (int q = 0; q < HESS_NB; q++)
+              if (q < i) a = a - Vp[r + (size_t)q * ldv] * s_w[q];
+            ac[r] = a;
+          }
+          if (r >= c + 2) nrm += abs2(a);
+          if (r == c + 1) *slot = a;
+        }
+      }
+      nrm = warp_sum(nrm);
+      if (lane == 0) redR[g] = nrm;
+    }
+    grid.sync();
+    // ---- (3) reflector (redundant per CTA), v, new column c ----
+    {
+      R t = 0;
+      for (int gg = tid; gg < G; gg += HP_TPB) t += redR[gg];
+      t = warp_sum(t);
+      if (lane == 0) s_rsum[warp] = t;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      R t = 0;
+#pragma unroll
+      for (int w8 = 0; w8 < HP_TPB / 32; w8++) t += s_rsum[w8];
+      S x0 = *slot;
+      if (t == R(0) && im(x0) == R(0)) {
+        s_tau = S(0); s_beta = x0; s_scal = S(0);
+      } else {
+        R nrmv = sqrt(abs2(x0) + t);
+        R b = re(x0) >= R(0) ? -nrmv : nrmv;
+        s_beta = mk<S>(b);
+        s_tau = (mk<S>(b) - x0) / mk<S>(b);
+        s_scal = S(1) / (x0 - mk<S>(b));
+      }
+    }
+    __syncthreads();
+    {
+      S* vc = V + (size_t)c * ldv;
+      const S scal = s_scal, beta = s_beta;
+      for (int s = g; s < nslab; s += G) {
+        const int r = s * HP_ROWS + tid;
+        if (tid < HP_ROWS && r < m && r >= c + 1) {
+          S a = ac[r];
+          vc[r] = (r == c + 1) ? S(1) : a * scal;
+          ac[r] = (r == c + 1) ? beta : S(0);
+        }
+      }
+      if (g == 0 && tid == 0) { tau[c] = s_tau; T[i + i * ldt] = s_tau; }
+    }
+    grid.sync();
+    // ---- (4) y = A[:, c+1:m] v over own rows; partials of V[:, 0:i]^H v ----
+    {
+      const S* vc = V + (size_t)c * ldv;
+      for (int q = c + 1 + tid; q < m; q += HP_TPB) sv[q] = vc[q];
+      __syncthreads();
+      S part[HESS_NB];
+#pragma unroll
+      for (int q = 0; q < HESS_NB; q++) part[q] = S(0);
+      for (int s = g; s < nslab; s += G) {
+        const int r = s * HP_ROWS + lane;
+        const int rr = r < m ? r : m - 1;
+        // each warp takes every NW-th column; UB coalesced 128-byte loads are issued
+        // back to back per iteration so enough bytes are in flight to cover L2/HBM latency
+        constexpr int NW = HP_TPB / 32, UB = sizeof(S) > 8 ? 8 : 32;
+        S acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u] = S(0);
+        int q = c + 1 + warp;
+        for (; q + NW * (UB - 1) < m; q += NW * UB) {
+          S a[UB];
+#pragma unroll
+          for (int u = 0; u < UB; u++) a[u] = A[rr + (size_t)(q + NW * u) * lda];
+#pragma unroll
+          for (int u = 0; u < UB; u++) acc[u & 7] = fmac(a[u], sv[q + NW * u], acc[u & 7]);
+        }
+        for (; q < m; q += NW) acc[0] = fmac(A[rr + (size_t)q * lda], sv[q], acc[0]);
+        s_part[warp][lane] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        __syncthreads();
+        if (tid < HP_ROWS && r < m) {
+          S y = S(0);
+#pragma unroll
+          for (int w = 0; w < HP_TPB / 32; w++) y += s_part[w][tid];
+          Y[r + (size_t)i * ldy] = y;  // unscaled, finished in (5)
+          if (i > 0 && r >= c + 1) {
+            const S vr = sv[r];
+#pragma unroll
+            for (int qq = 0; qq < HESS_NB; qq++)
+              if (qq < i) part[qq] = fmacc(Vp[r + (size_t)qq * ldv], vr, part[qq]);
+          }
+        }
+        __syncthreads();
+      }
+      if (warp == 0 && i > 0) {
+#pragma unroll
+        for (int qq = 0; qq < HESS_NB; qq++)
+          if (qq < i) {
+            S sum = warp_sum(part[qq]);
+            if (lane == 0) red2[g * HESS_NB + qq] = sum;
+          }
+      }
+    }
+    grid.sync();
+    // ---- (5) Y[:, i] = tau (y - Y[:, 0:i] u'), T[0:i, i] = -tau T u' ----
+    {
+      cta_sum_partials<S>(red2, G, i, s_u, s_part);
+      const S ti = s_tau;
+      for (int s = g; s < nslab; s += G) {
+        const int r = s * HP_ROWS + tid;
+        if (tid < HP_ROWS && r < m) {
+          S y = Y[r + (size_t)i * ldy];
+#pragma unroll
+          for (int q = 0; q < HESS_NB; q++)
+            if (q < i) y = y - Y[r + (size_t)q * ldy] * s_u[q];
+          Y[r + (size_t)i * ldy] = ti * y;
+        }
+      }
+      if (g == 0 && tid < i) {
+        S sum = S(0);
+        for (int q = tid; q < i; q++) sum = fmac(T[tid + q * ldt], s_u[q], sum);
+        T[tid + i * ldt] = -(ti * sum);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <class S>
 struct HessWs {
-  S *V, *Y, *T, *part, *tau, *W1, *W2;
+  S *V, *Y, *T, *part, *tau, *W1, *W2, *red1, *red2, *slot, *skp;
+  typename tr<S>::R* redR;
   static void carve(Arena& ar, int m, HessWs& w) {
     w.V = ar.get<S>((size_t)m * m);
     w.Y = ar.get<S>((size_t)m * HESS_NB);
@@ -201,8 +446,29 @@ struct HessWs {
     w.tau = ar.get<S>((size_t)m);
     w.W1 = ar.get<S>((size_t)HESS_NB * m);
     w.W2 = ar.get<S>((size_t)HESS_NB * m);
+    w.red1 = ar.get<S>((size_t)1024 * HESS_NB);
+    w.red2 = ar.get<S>((size_t)1024 * HESS_NB);
+    w.redR = ar.get<typename tr<S>::R>(1024);
+    w.slot = ar.get<S>(8);
+    w.skp = ar.get<S>((size_t)HESS_SPLITK * HESS_NB * m);
   }
 };
+
+// grid size of the cooperative panel kernel (0 if it cannot be co-resident)
+template <class S>
+int hess_coop_grid(int m) {
+  int dev, nsm, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = (size_t)m * sizeof(S);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(hess_panel_coop_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hess_panel_coop_kernel<S>, HP_TPB, smem) != cudaSuccess)
+    return 0;
+  // two Schur factorisations (A and B) run concurrently: leave room for both
+  int cap = std::min(per * nsm / 2, 128);
+  return std::min(cap, cdiv(m, HP_ROWS));
+}
 
 // In place: A -> H (upper Hessenberg), Q (m x m) = Q0.
 template <class S>
@@ -211,12 +477,23 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
   zero_kernel<S><<<cdiv((size_t)m * m, 256), 256, 0, st>>>((size_t)m * m, w.V);
   MSY_LAUNCH_CK();
   const int last = m - 3;  // last column that gets a reflector
+  const int G = getenv("MSY_HESS_NOCOOP") ? 0 : hess_coop_grid<S>(m);
   int np = 0;
   for (int k = 0; k <= last; k += HESS_NB, np++) {
     const int nbp = min(HESS_NB, last - k + 1);
     S* T = w.T + (size_t)np * HESS_NB * ldt;
     zero_kernel<S><<<cdiv(HESS_NB * HESS_NB, 256), 256, 0, st>>>((size_t)HESS_NB * HESS_NB, T);
-    for (int i = 0; i < nbp; i++) {
+    if (G > 0) {  // one persistent cooperative launch for the whole panel
+      S* Ap = A;
+      int mm = m, ldaa = lda, kk = k, nb_ = nbp, ldvv = ldv, ldyy = ldy, ldtt = ldt;
+      S *Vv = w.V, *Yy = w.Y, *Tt = T, *ta = w.tau, *r1 = w.red1, *r2 = w.red2, *sl = w.slot;
+      typename tr<S>::R* rR = w.redR;
+      void* args[] = {&mm, &Ap, &ldaa, &kk, &nb_, &Vv, &ldvv, &Yy, &ldyy, &Tt, &ldtt, &ta, &r1, &r2, &rR, &sl};
+      MSY_CK(cudaLaunchCooperativeKernel((const void*)hess_panel_coop_kernel<S>, dim3(G), dim3(HP_TPB), args,
+                                         (size_t)m * sizeof(S), st));
+      MSY_LAUNCH_CK();
+    }
+    for (int i = 0; i < nbp && G == 0; i++) {
       const int c = k + i;
       int nch = i > 0 ? cdiv(m - c, HESS_CHUNK) : 0;  // gemv for reflector i-1 covered columns c..m-1
       hess_col_kernel<S><<<1, HESS_TPB, 0, st>>>(m, A, lda, k, i, nbp, w.V, ldv, w.Y, ldy, T, ldt, w.part, nch, w.tau);
@@ -226,7 +503,7 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
       hess_gemv_kernel<S><<<dim3(cdiv(m, HESS_ROWS), nchn), HESS_ROWS, 0, st>>>(m, A, lda, c + 1, w.V + (size_t)c * ldv, w.part);
       MSY_LAUNCH_CK();
     }
-    {  // finish Y[:, nbp-1]
+    if (G == 0) {  // finish Y[:, nbp-1]
       int c = k + nbp;
       int nch = cdiv(m - c, HESS_CHUNK);
       hess_col_kernel<S><<<1, HESS_TPB, 0, st>>>(m, A, lda, k, nbp, nbp, w.V, ldv, w.Y, ldy, T, ldt, w.part, nch,
@@ -241,8 +518,8 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
       int rc = gemm<S>('N', 'C', m, nc, nbp, S(-1), w.Y, ldy, Vp + c1, ldv, S(1), A + (size_t)c1 * lda, lda, st);
       if (rc) return rc;
       // left: W1 = V[k+1:m,:]^H A[k+1:m, c1:m]; W2 = T^H W1; A -= V W2
-      rc = gemm<S>('C', 'N', nbp, nc, m - k - 1, S(1), Vp + (k + 1), ldv, A + (k + 1) + (size_t)c1 * lda, lda, S(0),
-                   w.W1, HESS_NB, st);
+      rc = gemm_splitk<S>('C', 'N', nbp, nc, m - k - 1, S(1), Vp + (k + 1), ldv, A + (k + 1) + (size_t)c1 * lda, lda,
+                          S(0), w.W1, HESS_NB, w.skp, HESS_SPLITK, st);
       if (rc) return rc;
       rc = gemm<S>('C', 'N', nbp, nc, nbp, S(1), T, ldt, w.W1, HESS_NB, S(0), w.W2, HESS_NB, st);
       if (rc) return rc;
@@ -263,8 +540,8 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
     const S* T = w.T + (size_t)p * HESS_NB * ldt;
     int r0 = k + 1, nr = m - r0;
     // Q[r0:m, r0:m] -= V T (V^H Q[r0:m, r0:m])
-    int rc = gemm<S>('C', 'N', nbp, nr, nr, S(1), Vp + r0, ldv, Q + r0 + (size_t)r0 * ldq, ldq, S(0), w.W1, HESS_NB,
-                     st);
+    int rc = gemm_splitk<S>('C', 'N', nbp, nr, nr, S(1), Vp + r0, ldv, Q + r0 + (size_t)r0 * ldq, ldq, S(0), w.W1,
+                            HESS_NB, w.skp, HESS_SPLITK, st);
     if (rc) return rc;
     rc = gemm<S>('N', 'N', nbp, nr, nbp, S(1), T, ldt, w.W1, HESS_NB, S(0), w.W2, HESS_NB, st);
     if (rc) return rc;

@@ -26,50 +26,25 @@ template <> struct MsCfg<cfloat> { static constexpr int W = 112, NB = 16; };
 template <> struct MsCfg<cdouble> { static constexpr int W = 80, NB = 10; };
 constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
 
-// correctly rounded reciprocal (cheaper than a full division on the critical path)
-__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
-__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
-template <class R> __device__ __forceinline__ cplx<R> rcp_rn(cplx<R> x) {
-  R d = rcp_rn(x.x * x.x + x.y * x.y);
-  return cplx<R>(x.x * d, -x.y * d);
-}
-
-// Householder reflector for a 2/3-vector, every lane computing it redundantly
-template <class S>
-__device__ __forceinline__ void refl3_fast(int nr, S x0, S x1, S x2, S& beta, S& tau, S& v1, S& v2) {
-  typedef typename tr<S>::R R;
-  R xn2 = abs2(x1) + (nr > 2 ? abs2(x2) : R(0));
-  if (xn2 == R(0) && im(x0) == R(0)) {
-    tau = S(0); beta = x0; v1 = S(0); v2 = S(0);
-    return;
-  }
-  R nrm = sqrt(abs2(x0) + xn2);
-  R b = re(x0) >= R(0) ? -nrm : nrm;
-  beta = mk<S>(b);
-  tau = (mk<S>(b) - x0) * mk<S>(rcp_rn(b));
-  S scal = rcp_rn(x0 - mk<S>(b));
-  v1 = x1 * scal;
-  v2 = nr > 2 ? x2 * scal : S(0);
-}
-
 // ---------------------------------------------------------------------------
 // window chase: one CTA, one warp per bulge, the W x W window of H and its
 // accumulated Z in shared memory.  Per step: every active bulge computes its
 // reflector (all lanes, broadcast reads), applies it from the left to the
 // window's rows (phase A), then from the right to the window's columns and
 // to Z (phase B).  Bulges sit 4 rows apart, so one step's bulges touch disjoint
-// rows/columns; the two phases order the only overlapping entries.
+// rows/columns; the two phases order the only overlapping entries.  The warp
+// ops are branch-free (warp_left3 / warp_right3 redirect idle lanes to a dummy
+// row/column of the smem window).
 template <class S>
 __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int hi, int nb,
-                                                     const typename tr<S>::R* __restrict__ shifts, int ws, int we,
-                                                     int t0, int t1, S* Zg) {
+                                                    const typename tr<S>::R* __restrict__ shifts, int ws, int we,
+                                                    int t0, int t1, S* Zg) {
   typedef typename tr<S>::R R;
-  constexpr int KM = (MsCfg<S>::W + 31) / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = we - ws;
-  const int ld = nw + 1;
-  S* Hw = (S*)smem_raw;
-  S* Zw = Hw + (size_t)ld * nw;
+  const int ld = nw + 1;                // row nw of every column is the dummy row
+  S* Hw = (S*)smem_raw;                 // nw rows x (nw + 1) columns (column nw is the dummy)
+  S* Zw = Hw + (size_t)ld * (nw + 1);   // nw rows x nw columns
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
 #define HW(i, j) Hw[(i) + (j) * ld]
 #define ZW(i, j) Zw[(i) + (j) * ld]
@@ -80,7 +55,6 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
   }
   __syncthreads();
   const int j = warp;  // bulge handled by this warp
-  const int span1 = hi - lo - 1;
   for (int t = t0; t < t1; t++) {
     const int p = lo - 1 + t - 4 * j;  // global position
     const bool act = (j < nb) && (p >= lo - 1) && (p <= hi - 2);
@@ -100,25 +74,15 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
       refl3_fast<S>(nr, x0, x1, x2, beta, tau, v1, v2);
       __syncwarp();
       if (!iszero(tau)) {
-        const S ctau = conj(tau);
-        S h0[KM], h1[KM], h2[KM];
-#pragma unroll
-        for (int k = 0; k < KM; k++) {
-          const int c = pl + 1 + lane + 32 * k;
-          if (c < nw) {
-            h0[k] = HW(pl + 1, c); h1[k] = HW(pl + 2, c); h2[k] = nr > 2 ? HW(pl + 3, c) : S(0);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < KM; k++) {
-          const int c = pl + 1 + lane + 32 * k;
-          if (c < nw) {
-            S w = fmacc(v1, h1[k], h0[k]);
-            if (nr > 2) w = fmacc(v2, h2[k], w);
-            w = ctau * w;
-            HW(pl + 1, c) = h0[k] - w;
-            HW(pl + 2, c) = h1[k] - v1 * w;
-            if (nr > 2) HW(pl + 3, c) = h2[k] - v2 * w;
+        if (nr == 3) {
+          warp_left3<S>(Hw, ld, pl + 1, pl + 1, nw - 1, nw, conj(tau), v1, v2, lane);
+        } else {
+          const S ctau = conj(tau);
+          for (int c = pl + 1 + lane; c < nw; c += 32) {
+            S h0 = HW(pl + 1, c), h1 = HW(pl + 2, c);
+            S w = ctau * fmacc(v1, h1, h0);
+            HW(pl + 1, c) = h0 - w;
+            HW(pl + 2, c) = h1 - v1 * w;
           }
         }
       }
@@ -131,34 +95,22 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
     __syncthreads();
     if (act && !iszero(tau)) {
       // rows of H touched: window rows 0..min(p+4,hi); rows of Z that can be nonzero:
-      // 0..(front bulge position + 3) -- rows below were never mixed in this pass
+      // 0..(position of bulge 0 + 3) -- bulge 0 leads the chain, even after it left at the
+      // bottom, and every row beyond it is still an identity row of Z
       const int rmax = ((p + 4 < hi) ? p + 4 : hi) - ws;
-      const int x = t - span1;
-      const int jh = x > 0 ? (x + 3) / 4 : 0;
-      const int zmax = min(nw - 1, (lo - 1 + t - 4 * jh) - ws + 3);
-#pragma unroll
-      for (int pass = 0; pass < 2; pass++) {
-        S* M = pass == 0 ? Hw : Zw;
-        const int last = pass == 0 ? rmax : zmax;
-        S a0[KM], a1[KM], a2[KM];
-#pragma unroll
-        for (int k = 0; k < KM; k++) {
-          const int r = lane + 32 * k;
-          if (r <= last) {
-            a0[k] = M[r + (pl + 1) * ld]; a1[k] = M[r + (pl + 2) * ld];
-            a2[k] = nr > 2 ? M[r + (pl + 3) * ld] : S(0);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < KM; k++) {
-          const int r = lane + 32 * k;
-          if (r <= last) {
-            S w = fmac(a1[k], v1, a0[k]);
-            if (nr > 2) w = fmac(a2[k], v2, w);
-            w = tau * w;
-            M[r + (pl + 1) * ld] = a0[k] - w;
-            M[r + (pl + 2) * ld] = a1[k] - w * conj(v1);
-            if (nr > 2) M[r + (pl + 3) * ld] = a2[k] - w * conj(v2);
+      const int zmax = min(nw - 1, (lo - 1 + t) - ws + 3);
+      if (nr == 3) {
+        warp_right3<S>(Hw, ld, pl + 1, 0, rmax, nw, tau, v1, v2, lane);
+        warp_right3<S>(Zw, ld, pl + 1, 0, zmax, nw, tau, v1, v2, lane);
+      } else {
+        for (int pass = 0; pass < 2; pass++) {
+          S* M = pass == 0 ? Hw : Zw;
+          const int last = pass == 0 ? rmax : zmax;
+          for (int r = lane; r <= last; r += 32) {
+            S a0 = M[r + (pl + 1) * ld], a1 = M[r + (pl + 2) * ld];
+            S w = tau * fmac(a1, v1, a0);
+            M[r + (pl + 1) * ld] = a0 - w;
+            M[r + (pl + 2) * ld] = a1 - w * conj(v1);
           }
         }
       }
@@ -282,10 +234,10 @@ int apply_z_regions(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int
   static bool attr = false;
   if (!attr) {
     MSY_CK(cudaFuncSetAttribute(apply_z_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)applyz_smem<S>(ZMAX)));
+                                (int)applyz_smem<S>(MsCfg<S>::W)));
     attr = true;
   }
-  if (nz > ZMAX) return -4;
+  if (nz > MsCfg<S>::W) return -4;
   int nblk = (cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
   if (nblk == 0) return 0;
   apply_z_kernel<S><<<nblk, 256, applyz_smem<S>(nz), st>>>(nz, Z, H, ldh, w0, cL0, cL1, rR1, U, ldu, U ? m : 0);
@@ -366,12 +318,19 @@ __global__ void __launch_bounds__(1024) scan_kernel(int m, S* H, int ldh, S* U, 
     if (tid == 0) { HH(i, l) = S(0); s_i = i - 2; }
     __syncthreads();
   }
+  // lo = start of the unreduced block ending at i: block-wide max over zero subdiagonals
+  __shared__ int s_lo;
+  if (tid == 0) s_lo = 0;
+  __syncthreads();
+  const int ifin = s_i;
+  int mylo = 0;
+  for (int k = 1 + tid; k <= ifin; k += nt)
+    if (iszero(HH(k, k - 1))) mylo = k;  // k increases with the stride: last hit is this thread's max
+  if (mylo) atomicMax(&s_lo, mylo);
+  __syncthreads();
   if (tid == 0) {
-    int i = s_i, lo = 0;
-    for (int k = i; k >= 1; k--)
-      if (iszero(HH(k, k - 1))) { lo = k; break; }
-    out[0] = i;
-    out[1] = i >= 0 ? lo : 0;
+    out[0] = ifin;
+    out[1] = ifin >= 0 ? s_lo : 0;
   }
 #undef HH
 }

@@ -12,6 +12,9 @@
 #include "multishift.cuh"
 #include "schur_small.cuh"
 
+#include <chrono>
+#include <cstdlib>
+
 namespace msy {
 
 template <class S>
@@ -37,6 +40,23 @@ struct SchurWs {
 
 struct SchurStats {
   int status, sweeps, small_calls, windows;
+  double ms_hess, ms_scan, ms_small, ms_shift, ms_sweep;  // filled when MSY_SCHUR_TIMING=1
+};
+
+// diagnostic phase timer: synchronises the stream at each mark (only when enabled)
+struct PhaseTimer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(cudaStream_t s) : on(getenv("MSY_SCHUR_TIMING") != nullptr), st(s) { t = now(); }
+  static std::chrono::steady_clock::time_point now() { return std::chrono::steady_clock::now(); }
+  void lap(double* acc) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    auto t2 = now();
+    *acc += std::chrono::duration<double, std::milli>(t2 - t).count();
+    t = t2;
+  }
 };
 
 // per-host-thread auxiliary stream + events used to overlap the window chases
@@ -69,7 +89,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
              cudaStream_t st, int* nwin) {
   constexpr int W = MsCfg<S>::W;
   static bool attr = false;
-  const size_t smem_max = (size_t)2 * (W + 1) * W * sizeof(S);
+  const size_t smem_max = (size_t)(W + 1) * (2 * W + 1) * sizeof(S);  // H window + dummy column, Z
   if (!attr) {
     MSY_CK(cudaFuncSetAttribute(chase_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
     attr = true;
@@ -104,7 +124,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
   auto chase = [&](int k) -> int {
     const Win& w = wins[k];
     int nw = w.we - w.ws;
-    chase_kernel<S><<<1, nthr, (size_t)2 * (nw + 1) * nw * sizeof(S), st>>>(H, ldh, lo, hi, nb, shifts, w.ws, w.we,
+    chase_kernel<S><<<1, nthr, (size_t)(nw + 1) * (2 * nw + 1) * sizeof(S), st>>>(H, ldh, lo, hi, nb, shifts, w.ws, w.we,
                                                                             w.t0, w.t1, Zbuf + (k & 1) * ZMAX * ZMAX);
     MSY_LAUNCH_CK();
     MSY_CK(cudaEventRecord(sc->evC, st));
@@ -140,7 +160,7 @@ template <class S>
 int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_t st, SchurStats* stats) {
   typedef typename tr<S>::R R;
   constexpr int NMIN = SmallCfg<S>::NMAX;
-  SchurStats loc = {0, 0, 0, 0};
+  SchurStats loc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (m <= NMIN) {
     int rc = schur_small_launch<S>(m, A, lda, U, ldu, SS_HESS | SS_WANTZ, nullptr, nullptr, w.dinfo, st);
     if (rc) return rc;
@@ -153,8 +173,10 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     if (stats) *stats = loc;
     return 0;
   }
+  PhaseTimer pt(st);
   int rc = hessenberg_blocked<S>(m, A, lda, U, ldu, w.hw, st);
   if (rc) return rc;
+  pt.lap(&loc.ms_hess);
   int hi = m - 1, stag = 0, last_hi = m;
   const int limit = 30 * m;
   while (true) {
@@ -165,6 +187,7 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     MSY_CK(cudaStreamSynchronize(st));
     hi = hinfo[0];
     int lo = hinfo[1];
+    pt.lap(&loc.ms_scan);
     if (hi < 0) break;
     if (hi < last_hi) { stag = 0; last_hi = hi; } else stag++;
     int sz = hi - lo + 1;
@@ -177,6 +200,7 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
       int sinfo[2];
       MSY_CK(cudaMemcpyAsync(sinfo, w.dinfo + 8, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
       MSY_CK(cudaStreamSynchronize(st));
+      pt.lap(&loc.ms_small);
       loc.small_calls++;
       loc.sweeps += sinfo[1];
       if (sinfo[0]) { loc.status = sinfo[0]; break; }
@@ -199,9 +223,10 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     }
     pair_shifts_kernel<S><<<1, 32, 0, st>>>(ns, w.wr, w.wi, nb, w.shifts, exc ? 1 : 0, A, lda, lo, hi, w.dinfo + 24);
     MSY_LAUNCH_CK();
-    // bulges whose shifts could not be paired reuse the last pair
+    pt.lap(&loc.ms_shift);
     rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, w.shifts, w.Z, st, &loc.windows);
     if (rc) return rc;
+    pt.lap(&loc.ms_sweep);
     loc.sweeps++;
   }
   if (stats) *stats = loc;

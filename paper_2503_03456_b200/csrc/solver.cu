@@ -652,6 +652,9 @@ static int schur_entry(int m, void* A, int lda, void* U, int ldu, void* ws, size
   if (rc) return rc;
   MSY_CK(cudaStreamSynchronize(st));
   if (info) { info[0] = s.status; info[1] = s.sweeps; info[2] = s.small_calls; info[3] = s.windows; }
+  if (getenv("MSY_SCHUR_TIMING"))
+    fprintf(stderr, "schur m=%d: hess %.1f ms, scan %.1f, small %.1f, shift %.1f, sweep %.1f\n", m, s.ms_hess,
+            s.ms_scan, s.ms_small, s.ms_shift, s.ms_sweep);
   return 0;
 }
 int sylv_schur(int dtype, int m, void* A, int lda, void* U, int ldu, void* ws, size_t ws_bytes, void* stream,
