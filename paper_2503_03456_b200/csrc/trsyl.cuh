@@ -79,8 +79,66 @@ __device__ bool small_solve(int nsys, S M[4][4], S rhs[4]) {
   return true;
 }
 
+// Solve the p x q unit system  TA_RR Y + Y TB_CC = W_RC  in registers (compile-time
+// sizes: fully unrolled Gaussian elimination with partial pivoting on the pq x pq
+// Kronecker matrix I (x) TA_RR + TB_CC^T (x) I).  Writes Y over W; false on an
+// exactly zero pivot (then Y = NaN).
+template <class S, int PP, int QQ>
+__device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int P, int i, int j) {
+  typedef typename tr<S>::R R;
+  constexpr int NS = PP * QQ;
+  S M[NS][NS], x[NS];
+#pragma unroll
+  for (int c = 0; c < QQ; c++)
+#pragma unroll
+    for (int r = 0; r < PP; r++) {
+      const int u = r + PP * c;
+      x[u] = Ws[(i + r) + (j + c) * P];
+#pragma unroll
+      for (int v = 0; v < NS; v++) M[u][v] = S(0);
+#pragma unroll
+      for (int r2 = 0; r2 < PP; r2++) M[u][r2 + PP * c] = M[u][r2 + PP * c] + As[(i + r) + (i + r2) * P];
+#pragma unroll
+      for (int c2 = 0; c2 < QQ; c2++) M[u][r + PP * c2] = M[u][r + PP * c2] + Bs[(j + c2) + (j + c) * P];
+    }
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < NS; c++) {
+    // partial pivoting by swapping values (indices stay compile-time constants)
+#pragma unroll
+    for (int r = c + 1; r < NS; r++) {
+      if (abs1(M[r][c]) > abs1(M[c][c])) {
+#pragma unroll
+        for (int v = 0; v < NS; v++) { S t = M[c][v]; M[c][v] = M[r][v]; M[r][v] = t; }
+        S t = x[c]; x[c] = x[r]; x[r] = t;
+      }
+    }
+    if (abs1(M[c][c]) == R(0)) ok = false;
+    const S inv = ok ? S(1) / M[c][c] : S(0);
+#pragma unroll
+    for (int r = c + 1; r < NS; r++) {
+      const S f = M[r][c] * inv;
+#pragma unroll
+      for (int v = c + 1; v < NS; v++) M[r][v] = M[r][v] - f * M[c][v];
+      x[r] = x[r] - f * x[c];
+    }
+  }
+#pragma unroll
+  for (int c = NS - 1; c >= 0; c--) {
+    S s = x[c];
+#pragma unroll
+    for (int v = c + 1; v < NS; v++) s = s - M[c][v] * x[v];
+    x[c] = s / M[c][c];
+  }
+#pragma unroll
+  for (int c = 0; c < QQ; c++)
+#pragma unroll
+    for (int r = 0; r < PP; r++) Ws[(i + r) + (j + c) * P] = ok ? x[r + PP * c] : mk<S>(NAN, NAN);
+  return ok;
+}
+
 template <class S>
-__global__ void __launch_bounds__(512) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
+__global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
                                                          const S* __restrict__ TB, int ldb, int lowerB, S* W, int ldw,
                                                          const int* __restrict__ rb, const int* __restrict__ cb, int nbi,
                                                          int nbj, int d, int* status) {
@@ -98,9 +156,9 @@ __global__ void __launch_bounds__(512) trsyl_step_kernel(int m, int n, const S* 
   S* As = (S*)smem_raw;      // [k][i], ld P   (K up to NB+1)
   S* Bs = As + P * P;        // [k][j], ld P
   S* Ws = Bs + P * P;        // W block, [i + j*P]
-  __shared__ int ru_start[NB + 2], ru_rank[NB + 2], cu_start[NB + 2], cu_rank[NB + 2];
+  __shared__ int ru_rank[NB + 2], cu_rank[NB + 2];
   __shared__ int ru_of[NB + 2], cu_of[NB + 2];  // rank -> first row / column of the unit
-  __shared__ int nru, ncu, s_fail;
+  __shared__ int nru, ncu;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int tr_ = tid % MT, tc = tid / MT;
   const bool mt_act = tid < MT * MT;
@@ -190,6 +248,11 @@ __global__ void __launch_bounds__(512) trsyl_step_kernel(int m, int n, const S* 
   }
   if (!solve) return;
   // ---- leaf: TA_II Y + Y TB_JJ = W_IJ in shared memory ----
+  // element-level anti-diagonal wavefront over 1x1 / 2x2 units: sub-step s solves the
+  // units (a, b) with a + b = s (a = row-unit rank from the bottom, b = column-unit
+  // rank in solve order), then every pending entry subtracts the contributions of
+  // the units just solved.  Entry ownership and unit ranks are precomputed, so a
+  // sub-step costs a few shared-memory FMAs per owned entry plus two barriers.
   for (int e = tid; e < bi * bi; e += nt) {
     int i = e % bi, k = e / bi;
     As[i + k * P] = TA[(i0 + i) + (size_t)(i0 + k) * lda];
@@ -199,13 +262,15 @@ __global__ void __launch_bounds__(512) trsyl_step_kernel(int m, int n, const S* 
     Bs[i + k * P] = TB[(j0 + i) + (size_t)(j0 + k) * ldb];
   }
   __syncthreads();
+  __shared__ int ru_len[NB + 2], cu_len[NB + 2];
   if (tid == 0) {
     // row units from the bottom (rank 0 = bottom unit); 2x2 if As[i][i-1] != 0
     int cnt = 0, i = bi - 1;
     while (i >= 0) {
       int st = (i > 0 && !iszero(As[i + (i - 1) * P])) ? i - 1 : i;
-      for (int q = st; q <= i; q++) { ru_start[q] = st; ru_rank[q] = cnt; }
+      for (int q = st; q <= i; q++) ru_rank[q] = cnt;
       ru_of[cnt] = st;
+      ru_len[cnt] = i - st + 1;
       cnt++;
       i = st - 1;
     }
@@ -216,8 +281,9 @@ __global__ void __launch_bounds__(512) trsyl_step_kernel(int m, int n, const S* 
       int j = 0;
       while (j < bj) {
         int len = (j + 1 < bj && !iszero(Bs[(j + 1) + j * P])) ? 2 : 1;
-        for (int q = j; q < j + len; q++) { cu_start[q] = j; cu_rank[q] = cnt; }
+        for (int q = j; q < j + len; q++) cu_rank[q] = cnt;
         cu_of[cnt] = j;
+        cu_len[cnt] = len;
         cnt++;
         j += len;
       }
@@ -225,69 +291,76 @@ __global__ void __launch_bounds__(512) trsyl_step_kernel(int m, int n, const S* 
       int j = bj - 1;
       while (j >= 0) {
         int st = (j > 0 && !iszero(Bs[(j - 1) + j * P])) ? j - 1 : j;
-        for (int q = st; q <= j; q++) { cu_start[q] = st; cu_rank[q] = cnt; }
+        for (int q = st; q <= j; q++) cu_rank[q] = cnt;
         cu_of[cnt] = st;
+        cu_len[cnt] = j - st + 1;
         cnt++;
         j = st - 1;
       }
     }
     ncu = cnt;
-    s_fail = 0;
   }
   __syncthreads();
+  constexpr int EPT = ((NB + 1) * (NB + 1) + 511) / 512;  // entries per thread (512 threads)
+  int ei[EPT], ej[EPT], era[EPT], ecr[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; k++) {
+    const int e = tid + k * nt;
+    if (e < bi * bj) {
+      ei[k] = e % bi; ej[k] = e / bi;
+      era[k] = ru_rank[ei[k]]; ecr[k] = cu_rank[ej[k]];
+    } else {
+      ei[k] = 0; ej[k] = 0; era[k] = -1000000; ecr[k] = -1000000;  // never pending
+    }
+  }
   const int nsteps = nru + ncu - 1;
   for (int s = 0; s < nsteps; s++) {
-    // phase 1: solve the units on anti-diagonal s (one thread per unit, indexed by row unit rows)
-    for (int i = tid; i < bi; i += nt) {
-      if (ru_start[i] != i) continue;  // one thread per row unit (its first row)
-      int ra = ru_rank[i], cr = s - ra;
-      if (cr < 0 || cr >= ncu) continue;
-      int jst = cu_of[cr];
-      int p = (i + 1 < bi && ru_start[i + 1] == i) ? 2 : 1;
-      int q = (jst + 1 < bj && cu_start[jst + 1] == jst) ? 2 : 1;
-      S M[4][4], rhs[4];
-      int ns = p * q;
-      for (int a = 0; a < 4; a++)
-        for (int b = 0; b < 4; b++) M[a][b] = S(0);
-      // unknown index u = r + p*c  (vec, column-major over the unit)
-      for (int c = 0; c < q; c++)
-        for (int r = 0; r < p; r++) {
-          int uu = r + p * c;
-          rhs[uu] = Ws[(i + r) + (jst + c) * P];
-          for (int r2 = 0; r2 < p; r2++) M[uu][r2 + p * c] += As[(i + r) + (i + r2) * P];      // TA_RR Y
-          for (int c2 = 0; c2 < q; c2++) M[uu][r + p * c2] += Bs[(jst + c2) + (jst + c) * P];  // Y TB_CC
+    // phase 1: thread a solves unit (a, s - a)
+    if (tid < nru) {
+      const int a = tid, bb = s - a;
+      if (bb >= 0 && bb < ncu) {
+        const int i = ru_of[a], p = ru_len[a], jst = cu_of[bb], q = cu_len[bb];
+        bool ok = true;
+        if (p == 1 && q == 1) {
+          const S d = As[i + i * P] + Bs[jst + jst * P];
+          ok = !iszero(d);
+          Ws[i + jst * P] = ok ? Ws[i + jst * P] / d : mk<S>(NAN, NAN);
+        } else if (p == 2 && q == 1) {
+          ok = unit_solve<S, 2, 1>(As, Bs, Ws, P, i, jst);
+        } else if (p == 1 && q == 2) {
+          ok = unit_solve<S, 1, 2>(As, Bs, Ws, P, i, jst);
+        } else {
+          ok = unit_solve<S, 2, 2>(As, Bs, Ws, P, i, jst);
         }
-      if (!small_solve<S>(ns, M, rhs)) {
-        // singular diagonal pair: report the first in reference order
-        int jg = j0 + jst, ig = i0 + i + p - 1;
-        int crank = lowerB ? (n - 1 - jg) : jg;
-        atomicMin(&status[0], crank * m + (m - 1 - ig));  // decoded on the host
-        for (int uu = 0; uu < ns; uu++) rhs[uu] = mk<S>(NAN, NAN);
+        if (!ok) {  // singular diagonal pair: report the first in reference order (decoded on the host)
+          const int jg = j0 + jst, ig = i0 + i + p - 1;
+          const int crank = lowerB ? (n - 1 - jg) : jg;
+          atomicMin(&status[0], crank * m + (m - 1 - ig));
+        }
       }
-      for (int c = 0; c < q; c++)
-        for (int r = 0; r < p; r++) Ws[(i + r) + (jst + c) * P] = rhs[r + p * c];
     }
     __syncthreads();
-    // phase 2: pending entries take the contributions of the units just solved
-    for (int e = tid; e < bi * bj; e += nt) {
-      int i = e % bi, j = e / bi;
-      int ra = ru_rank[i], cr = cu_rank[j];
-      if (ra + cr <= s) continue;
-      S v = Ws[i + j * P];
-      // solved unit in my column unit: row rank s - cr (below me if < ra)
-      int rs = s - cr;
-      if (rs >= 0 && rs < ra) {
-        int st = ru_of[rs];
-        int len = (st + 1 < bi && ru_start[st + 1] == st) ? 2 : 1;
-        for (int k = st; k < st + len; k++) v = v - As[i + k * P] * Ws[k + j * P];
+    // phase 2: owned pending entries take the contributions of the units just solved
+#pragma unroll
+    for (int k = 0; k < EPT; k++) {
+      const int ra = era[k], cr = ecr[k];
+      if (ra + cr > s) {
+        const int i = ei[k], j = ej[k];
+        S v = Ws[i + j * P];
+        const int rs = s - cr;  // solved unit in my column unit (below me if rs < ra)
+        if (rs >= 0 && rs < ra) {
+          const int st = ru_of[rs];
+          v = v - As[i + st * P] * Ws[st + j * P];
+          if (ru_len[rs] == 2) v = v - As[i + (st + 1) * P] * Ws[(st + 1) + j * P];
+        }
+        const int cs = s - ra;  // solved unit in my row unit (before me if cs < cr)
+        if (cs >= 0 && cs < cr) {
+          const int st = cu_of[cs];
+          v = v - Ws[i + st * P] * Bs[st + j * P];
+          if (cu_len[cs] == 2) v = v - Ws[i + (st + 1) * P] * Bs[(st + 1) + j * P];
+        }
+        Ws[i + j * P] = v;
       }
-      int cs = s - ra;
-      if (cs >= 0 && cs < cr) {
-        int st = cu_of[cs];
-        int len = (st + 1 < bj && cu_start[st + 1] == st) ? 2 : 1;
-        for (int k = st; k < st + len; k++) v = v - Ws[i + k * P] * Bs[k + j * P];
-      }
-      Ws[i + j * P] = v;
     }
     __syncthreads();
   }
