@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
       } else {
         x0 = HW(pl + 1, pl); x1 = HW(pl + 2, pl); x2 = nr > 2 ? HW(pl + 3, pl) : S(0);
       }
-      refl3_fast<S>(nr, x0, x1, x2, beta, tau, v1, v2);
+      refl3_fast(nr, x0, x1, x2, beta, tau, v1, v2);
       __syncwarp();
       if (!iszero(tau)) {
         if (nr == 3) {
