@@ -28,6 +28,7 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context (see batch.py)
 sys.path.insert(0, ROOT)
 
 METRIC = "mixed-precision Sylvester solves/sec at m=n=4096"
@@ -47,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-m", type=int, default=512)
+    ap.add_argument("--batch", type=int, default=512, help="c4: equations per job (all ranks together)")
+    ap.add_argument("--lanes", type=int, default=0, help="c4: concurrent solves per GPU (0 = library default)")
     return ap.parse_args()
 
 
@@ -173,6 +176,57 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+
+# ---------------------------------------------------------------------------
+def dmma_roofline(L, st, dev, m):
+    """Live roofline of the dominant kernel class: the fp64 DMMA GEMM engine (CUDA events on its stream)."""
+    import torch
+    pk = {}
+    for kind, name in ((0, "ffma"), (1, "dfma"), (2, "dmma")):
+        v = ct.c_double()
+        if L.sylv_microbench(kind, ct.byref(v), ct.c_void_p(st.cuda_stream)) == 0:
+            pk[name] = v.value
+    g = 4096 if m >= 4096 else max(m, 1024)
+    Ga = torch.randn(g, g, dtype=torch.float64, device=dev)
+    Gb = torch.randn(g, g, dtype=torch.float64, device=dev)
+    Gc = torch.empty(g, g, dtype=torch.float64, device=dev)
+    one, zero = ct.c_double(1.0), ct.c_double(0.0)
+
+    def dgemm():
+        return L.sylv_gemm(1, b"N", b"N", g, g, g, ct.byref(one), Ga.data_ptr(), g, Gb.data_ptr(), g,
+                           ct.byref(zero), Gc.data_ptr(), g, ct.c_void_p(st.cuda_stream))
+
+    for _ in range(3):
+        dgemm()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(st)
+    nrep = 5
+    for _ in range(nrep):
+        dgemm()
+    a1.record(st)
+    a1.synchronize()
+    gms = a0.elapsed_time(a1) / nrep
+    achieved = 2.0 * g ** 3 / (gms * 1e-3) / 1e12
+    peak = pk.get("dmma")
+    roof = {"bound": "tensor", "kernel": "gemm_dmma_kernel (fp64 DMMA.8x8x4)", "achieved": achieved,
+            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+            "peak_source": "measured live by sylv_microbench(DMMA) (MEASURED_PEAKS.json has no fp64)",
+            "algorithmic": f"2*{g}^3 flop per launch ({g}^3 GEMM), {gms:.2f} ms per launch"}
+    return roof, pk
+
+
+def solve_roofline(pk, variant, kind, m, n, k, cx, t_step, solves_per_step):
+    """Paper flop counts (costmodel.flops: low 25a+b fp32, high 6a+(4+3k)b fp64) against the measured peaks."""
+    from paper_2503_03456_b200.costmodel import algorithm_name, flops, gemm_phase_flops
+    fc = flops(algorithm_name(variant, kind), m, n, k)
+    mult = (4.0 if cx else 1.0) * solves_per_step
+    low, high = fc.low_flops * mult, fc.high_flops * mult
+    p32, p64 = pk.get("ffma"), pk.get("dmma")
+    lb = (low / (p32 * 1e12) + high / (p64 * 1e12)) if p32 and p64 else None
+    return {"low_flops": low, "high_flops": high, "gflops": (low + high) / t_step / 1e9,
+            "frac_of_fp32_fp64_roofline": (lb / t_step) if lb else None,
+            "peaks_tflops": pk, "gemm_phase_fp64_flops": gemm_phase_flops(m, n, k) * mult}
+
 # ---------------------------------------------------------------------------
 def run_ours(args):
     import numpy as np
@@ -185,8 +239,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     import paper_2503_03456_b200 as M
     from paper_2503_03456_b200 import _native, problems as P
-    from paper_2503_03456_b200.costmodel import algorithm_name, flops, gemm_phase_flops
     L = _native.lib()
+    peaks = measured_peaks()
     fm, fn = P.FULL_SIZES[args.config]
     fm, fn = args.m or fm, args.n or fn
     if args.config == "c4":
@@ -263,54 +317,12 @@ def run_ours(args):
         e2e = {"value": world * ne / (tot / 1e3), "unit": "solves/s",
                "h2d_bytes_per_step": (m * m + n * n + m * n) * esz, "d2h_bytes_per_step": m * n * esz}
     # ---- roofline: the fp64 DMMA GEMM engine of the contraction phases, timed live ----
-    peaks = measured_peaks()
-    roof = None
-    sol_roof = None
+    roof = sol_roof = None
     if rank == 0:
-        pk = {}
-        for kind, name in ((0, "ffma"), (1, "dfma"), (2, "dmma")):
-            v = ct.c_double()
-            if L.sylv_microbench(kind, ct.byref(v), ct.c_void_p(st.cuda_stream)) == 0:
-                pk[name] = v.value
-        g = 4096 if m >= 4096 else max(m, 1024)
-        Ga = torch.randn(g, g, dtype=torch.float64, device=dev)
-        Gb = torch.randn(g, g, dtype=torch.float64, device=dev)
-        Gc = torch.empty(g, g, dtype=torch.float64, device=dev)
-        one, zero = ct.c_double(1.0), ct.c_double(0.0)
-
-        def dgemm():
-            return L.sylv_gemm(1, b"N", b"N", g, g, g, ct.byref(one), Ga.data_ptr(), g, Gb.data_ptr(), g,
-                               ct.byref(zero), Gc.data_ptr(), g, ct.c_void_p(st.cuda_stream))
-
-        for _ in range(3):
-            dgemm()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(st)
-        nrep = 5
-        for _ in range(nrep):
-            dgemm()
-        a1.record(st)
-        a1.synchronize()
-        gms = a0.elapsed_time(a1) / nrep
-        achieved = 2.0 * g ** 3 / (gms * 1e-3) / 1e12
-        peak = pk.get("dmma")
-        roof = {"bound": "tensor", "kernel": "gemm_dmma_kernel (fp64 DMMA.8x8x4)", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
-                "peak_source": "measured live by sylv_microbench(DMMA) (MEASURED_PEAKS.json has no fp64)",
-                "algorithmic": f"2*{g}^3 flop per launch ({g}^3 GEMM), {gms:.2f} ms per launch"}
-        alg = algorithm_name(args.variant, pr.kind)
-        fc = flops(alg, m, n, k)
-        mult = 4.0 if cx else 1.0
-        low, high = fc.low_flops * mult, fc.high_flops * mult
-        t_step = total_ms / args.steps / 1e3
-        p32, p64 = pk.get("ffma"), pk.get("dmma")
-        lb = (low / (p32 * 1e12) + high / (p64 * 1e12)) if p32 and p64 else None
-        sol_roof = {"low_flops": low, "high_flops": high, "gflops": (low + high) / t_step / 1e9,
-                    "frac_of_fp32_fp64_roofline": (lb / t_step) if lb else None,
-                    "peaks_tflops": pk, "gemm_phase_fp64_flops": gemm_phase_flops(m, n, k) * mult,
-                    "phase_ms": {"schur": reps[-1].ms_schur, "orth": reps[-1].ms_orth, "setup": reps[-1].ms_setup,
-                                 "y0": reps[-1].ms_y0, "refine": reps[-1].ms_refine,
-                                 "recover": reps[-1].ms_recover}}
+        roof, pk = dmma_roofline(L, st, dev, m)
+        sol_roof = solve_roofline(pk, args.variant, pr.kind, m, n, k, cx, total_ms / args.steps / 1e3, 1)
+        sol_roof["phase_ms"] = {"schur": reps[-1].ms_schur, "orth": reps[-1].ms_orth, "setup": reps[-1].ms_setup,
+                                "y0": reps[-1].ms_y0, "refine": reps[-1].ms_refine, "recover": reps[-1].ms_recover}
     # ---- CPU baseline (oracle port, rank 0 at N=1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -342,10 +354,133 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+def run_c4(args):
+    """C4: `batch` independent equations (config-0 recipe, m=n=512, entropy seed+i), sharded by equation
+    index over the ranks; each rank solves its block with the lane executor (sylv_solve_batched), then one
+    gather of X to rank 0 (the only collective).  Total work is fixed as N grows: scaling "strong"."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank, local, world = dist_info()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2503_03456_b200 as M
+    from paper_2503_03456_b200 import _native, problems as P
+    from paper_2503_03456_b200.batch import gather_solutions, shard_range
+    L = _native.lib()
+    peaks = measured_peaks()
+    m = args.m or P.FULL_SIZES["c4"][0]
+    total = args.batch
+    lo, hi = shard_range(total, rank, world)
+    cnt = hi - lo
+    probs = [P.make_c4(i, m) for i in range(lo, hi)]
+    hA = torch.stack([torch.as_tensor(p.A) for p in probs]).pin_memory()
+    hB = torch.stack([torch.as_tensor(p.B) for p in probs]).pin_memory()
+    hC = torch.stack([torch.as_tensor(p.C) for p in probs]).pin_memory()
+    A, B, C = hA.to(dev), hB.to(dev), hC.to(dev)
+    X = torch.empty_like(C)
+    hX = torch.empty_like(hC).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+
+    def step():
+        _, reps = M.solve_batched(A, B, C, out=X, lanes=args.lanes)
+        if world > 1:
+            gather_solutions(X, total)
+        return reps
+
+    for _ in range(args.warmup):
+        reps = step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = L.sylv_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            evs[i][0].record(st)
+            reps = step()
+            evs[i][1].record(st)
+        torch.cuda.synchronize(dev)
+    launches = (L.sylv_launch_count() - launches0) // max(1, args.steps)
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = t.item()
+    value = args.steps * total / (total_ms / 1e3)
+    ks = sorted({r.iterations for r in reps})
+    st_bad = sum(1 for r in reps if r.status != 0)
+    be = max(r.backward_error for r in reps)
+    # ---- e2e: pinned host inputs -> device, batched solve, X -> host, gather ----
+    e2e = None
+    if not args.no_e2e:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for i in range(max(1, args.steps)):
+            flush.fill_(float(i))
+            e0.record(st)
+            A.copy_(hA, non_blocking=True)
+            B.copy_(hB, non_blocking=True)
+            C.copy_(hC, non_blocking=True)
+            M.solve_batched(A, B, C, out=X, lanes=args.lanes)
+            hX.copy_(X, non_blocking=True)
+            if world > 1:
+                gather_solutions(X, total)
+            e1.record(st)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([tot], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = t.item()
+        es = hA.element_size()
+        e2e = {"value": max(1, args.steps) * total / (tot / 1e3), "unit": "solves/s",
+               "h2d_bytes_per_step": cnt * 3 * m * m * es, "d2h_bytes_per_step": cnt * m * m * es}
+    roof = sol_roof = cpu = None
+    if rank == 0:
+        roof, pk = dmma_roofline(L, st, dev, m)
+        sol_roof = solve_roofline(pk, "orth", "general", m, m, max(ks), False, total_ms / args.steps / 1e3,
+                                  cnt)
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_oracle(min(args.cpu_sample_m, m), m, m, threads=1)
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": f"mixed-precision Sylvester solves/sec (c4: {total} equations, m=n={m})",
+            "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded Philox, entropy seed+index)",
+            "config": {"workload": f"c4: {total} x real general m=n={m}, mp_orth binary32/binary64, the whole "
+                                   f"batch per step, sharded by equation index + gather of X to rank 0",
+                       "m": m, "n": m, "batch": total, "per_rank": cnt, "lanes": args.lanes or 16,
+                       "iterations": ks, "failed": st_bad, "max_backward_error": be,
+                       "lane_phase_ms_mean": {f: round(sum(getattr(r, "ms_" + f) for r in reps) / len(reps), 2)
+                                              for f in ("schur", "orth", "setup", "y0", "refine", "recover",
+                                                        "total")},
+                       "l2": "flushed between steps (256 MiB write); per-rank working set >> 126 MB L2",
+                       "parallelism": f"shard x{world} + gather"},
+            "roofline": roof, "solve_roofline": sol_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
+            "gpu_launches": int(launches),
+            "measured_peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c4":
+        run_c4(args)
     else:
         run_ours(args)
 

@@ -102,6 +102,23 @@ int sylv_workspace_size(const sylv_params* p, size_t* bytes);
 int sylv_solve(const sylv_params* p, const void* A, int lda, const void* B, int ldb, const void* C, int ldc,
                void* X, int ldx, void* ws, size_t ws_bytes, void* stream, sylv_report* rep);
 
+/* Batched solve of `batch` independent equations sharing *p (config C4: 512 x
+ * mp_orth at m = n = 512).  The reference solves them one by one through
+ * mp_orth / mp_inv (refinement.py:205-297; "independent solves may run
+ * concurrently"); here `lanes` of them run concurrently, each
+ * lane with its own stream, host worker and workspace slice.  A, B, C, X are host
+ * arrays of `batch` device pointers (column-major, leading dimensions shared);
+ * reports is a host array of `batch` records.  lanes <= 0 selects the default
+ * (32).  Each lane keeps its equation's work on one stream, so the process
+ * should create its CUDA context with CUDA_DEVICE_MAX_CONNECTIONS >= lanes
+ * (the Python package sets 32) or lanes share hardware queues.  The call
+ * returns when every equation is done; `stream` is ordered before and after
+ * the batch. */
+int sylv_batched_workspace_size(const sylv_params* p, int lanes, size_t* bytes);
+int sylv_solve_batched(const sylv_params* p, int batch, const void* const* A, int lda, const void* const* B, int ldb,
+                       const void* const* C, int ldc, void* const* X, int ldx, int lanes, void* ws, size_t ws_bytes,
+                       void* stream, sylv_report* reports);
+
 /* solve_pert_sylv_tri_stat (refinement.py:95-141): stationary refinement of
  * (T_A + dT_A) Y + Y (T_B + dT_B) = C in binary64; T_A upper (quasi-)
  * triangular, T_B upper or lower (quasi-)triangular. dtype 1 or 3. */

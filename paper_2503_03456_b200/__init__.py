@@ -7,6 +7,12 @@ exception types, backed by hand-written sm_100a CUDA kernels behind the C ABI
 in ``include/mpsylv_b200.h``.  ``solve`` is the torch-native entry.
 """
 
+import os as _os
+
+# one hardware work queue per stream for the batched lane executor (C4): must be in the
+# environment before the CUDA context exists, i.e. before torch touches the device
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .costmodel import FlopCount, flops
 from .errors import (DeviceError, DimensionError, FormatOverflowError, IterationLimitError, MpsylvError,
                      NotHermitianError, NumericBreakdownError, PrecisionOverflowWarning, RankDeficiencyError,
@@ -14,6 +20,7 @@ from .errors import (DeviceError, DimensionError, FormatOverflowError, Iteration
 from .precision import (B24, BFLOAT16, BINARY16, BINARY32, BINARY64, FORMATS, TF32, FlopCounter, FpFormat,
                         PrecisionContext, format_from_name, parse_format)
 from .refinement import RefinementConfig, SolveReport, mp_inv, mp_orth, solve, solve_pert_sylv_tri_stat
+from .batch import gather_solutions, shard_range, solve_batched
 from .sylvester import SylvesterProblem, residual, solve_sylv_tri
 from .linalg import QrFactors, SchurFactors, gemm, mgs_qr, schur
 

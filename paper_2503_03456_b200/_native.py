@@ -26,7 +26,7 @@ DTYPE = {"float32": 0, "float64": 1, "complex64": 2, "complex128": 3}
 
 EXPORTS = (
     "sylv_version", "sylv_status_string", "sylv_launch_count", "sylv_microbench",
-    "sylv_workspace_size", "sylv_solve",
+    "sylv_workspace_size", "sylv_solve", "sylv_batched_workspace_size", "sylv_solve_batched",
     "sylv_refine_workspace_size", "sylv_refine", "sylv_schur_workspace_size", "sylv_schur",
     "sylv_trsyl_workspace_size", "sylv_trsyl", "sylv_orth_workspace_size", "sylv_orth", "sylv_gemm",
 )
@@ -76,6 +76,10 @@ def lib():
         L.sylv_workspace_size.argtypes = [ct.POINTER(Params), ct.POINTER(sz)]
         L.sylv_solve.argtypes = [ct.POINTER(Params), vp, ip, vp, ip, vp, ip, vp, ip, vp, sz, vp,
                                  ct.POINTER(Report)]
+        L.sylv_batched_workspace_size.argtypes = [ct.POINTER(Params), ip, ct.POINTER(sz)]
+        L.sylv_solve_batched.argtypes = [ct.POINTER(Params), ip, ct.POINTER(vp), ip, ct.POINTER(vp), ip,
+                                         ct.POINTER(vp), ip, ct.POINTER(vp), ip, ip, vp, sz, vp,
+                                         ct.POINTER(Report)]
         L.sylv_refine_workspace_size.argtypes = [ip, ip, ip, ct.POINTER(sz)]
         L.sylv_refine.argtypes = [ip, ip, ip, vp, ip, vp, ip, vp, ip, vp, ip, ip, vp, ip, vp, ip, dp, ip, vp, ip,
                                   vp, sz, vp, ct.POINTER(Report)]

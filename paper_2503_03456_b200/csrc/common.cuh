@@ -5,6 +5,8 @@
 // Scalar codes (the C-ABI `dtype`): 0 = float (s), 1 = double (d),
 // 2 = complex<float> (c), 3 = complex<double> (z).
 #pragma once
+#include <atomic>
+#include <cstring>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -186,6 +188,54 @@ inline unsigned long long& launch_counter() {
   do {                                                    \
     __atomic_add_fetch(&msy::launch_counter(), 1ULL, __ATOMIC_RELAXED); \
     MSY_CK(cudaGetLastError());                           \
+  } while (0)
+
+// Host waits of the solve path.  Interactive solves spin (lowest latency); the
+// batched executor's lanes switch to blocking-sync events so that dozens of host
+// threads waiting on their streams do not burn the host cores.
+inline bool& host_sync_blocking() {
+  thread_local bool b = false;
+  return b;
+}
+inline cudaError_t host_sync(cudaStream_t st) {
+  if (!host_sync_blocking()) return cudaStreamSynchronize(st);
+  thread_local cudaEvent_t ev = nullptr;
+  if (!ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventBlockingSync | cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaEventRecord(ev, st);
+  if (e != cudaSuccess) return e;
+  return cudaEventSynchronize(ev);
+}
+
+// Small device -> host readbacks (status words, norms) go through a per-thread
+// pinned staging buffer: a copy into pageable memory would make the driver stage
+// it synchronously, which serialises concurrent solve lanes.
+inline cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  thread_local void* pinned = nullptr;
+  constexpr size_t kCap = 4096;
+  if (bytes > kCap) return cudaErrorInvalidValue;
+  if (!pinned) {
+    cudaError_t e = cudaHostAlloc(&pinned, kCap, cudaHostAllocPortable);
+    if (e != cudaSuccess) { pinned = nullptr; return e; }
+  }
+  cudaError_t e = cudaMemcpyAsync(pinned, src, bytes, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return e;
+  e = host_sync(st);
+  if (e != cudaSuccess) return e;
+  memcpy(dst, pinned, bytes);
+  return cudaSuccess;
+}
+
+// one-time kernel attribute setup, safe under concurrent first calls
+#define MSY_SMEM_ATTR_ONCE(kern, bytes)                                                             \
+  do {                                                                                              \
+    static std::atomic<int> done__{0};                                                              \
+    if (!done__.load(std::memory_order_acquire)) {                                                  \
+      MSY_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))); \
+      done__.store(1, std::memory_order_release);                                                   \
+    }                                                                                               \
   } while (0)
 
 __host__ __device__ static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }

@@ -190,8 +190,8 @@ int lu_factor(int m, S* A, int lda, LuWs<S>& w, cudaStream_t st) {
 
 template <class S>
 int lu_read_status(LuWs<S>& w, int* singular, cudaStream_t st) {
-  MSY_CK(cudaMemcpyAsync(singular, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  MSY_CK(cudaStreamSynchronize(st));
+  MSY_CK(d2h(singular, w.flag, sizeof(int), st));
+  MSY_CK(host_sync(st));
   return 0;
 }
 

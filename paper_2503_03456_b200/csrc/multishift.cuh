@@ -231,12 +231,7 @@ static size_t applyz_smem(int nz) {
 template <class S>
 int apply_z_regions(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int w0, int cL0, int cL1, int rR1,
                     cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    MSY_CK(cudaFuncSetAttribute(apply_z_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)applyz_smem<S>(MsCfg<S>::W)));
-    attr = true;
-  }
+  MSY_SMEM_ATTR_ONCE(apply_z_kernel<S>, (int)applyz_smem<S>(MsCfg<S>::W));
   if (nz > MsCfg<S>::W) return -4;
   int nblk = (cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
   if (nblk == 0) return 0;

@@ -11,6 +11,7 @@
 #include "hessenberg.cuh"
 #include "multishift.cuh"
 #include "schur_small.cuh"
+#include "schur_mss.cuh"
 
 #include <chrono>
 #include <cstdlib>
@@ -52,31 +53,34 @@ struct PhaseTimer {
   static std::chrono::steady_clock::time_point now() { return std::chrono::steady_clock::now(); }
   void lap(double* acc) {
     if (!on) return;
-    cudaStreamSynchronize(st);
+    host_sync(st);
     auto t2 = now();
     *acc += std::chrono::duration<double, std::milli>(t2 - t).count();
     t = t2;
   }
 };
 
-// per-host-thread auxiliary stream + events used to overlap the window chases
-// (one CTA) with the off-window Z applications (many CTAs)
+// auxiliary stream + events used to overlap the window chases (one CTA) with the
+// off-window Z applications (many CTAs).  Owned by a solve lane (solver.cu) or,
+// for direct sylv_schur calls, by the calling host thread.
 struct SweepCtx {
-  cudaStream_t aux = nullptr;
+  cudaStream_t aux = nullptr;  // nullptr: serial mode (everything on the caller's stream)
   cudaEvent_t evC = nullptr, evN = nullptr, evD = nullptr;
   int dev = -1;
+  void ensure() {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (aux != nullptr && dev == d) return;
+    cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&evC, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evN, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evD, cudaEventDisableTiming);
+    dev = d;
+  }
 };
 inline SweepCtx* sweep_ctx() {
   thread_local SweepCtx c;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (c.aux == nullptr || c.dev != dev) {
-    cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&c.evC, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&c.evN, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&c.evD, cudaEventDisableTiming);
-    c.dev = dev;
-  }
+  c.ensure();
   return &c;
 }
 
@@ -86,15 +90,10 @@ inline SweepCtx* sweep_ctx() {
 // on `aux`; the near part (columns the next window will load) runs first.
 template <class S>
 int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const typename tr<S>::R* shifts, S* Zbuf,
-             cudaStream_t st, int* nwin) {
+             cudaStream_t st, int* nwin, SweepCtx* sc) {
   constexpr int W = MsCfg<S>::W;
-  static bool attr = false;
   const size_t smem_max = (size_t)(W + 1) * (2 * W + 1) * sizeof(S);  // H window + dummy column, Z
-  if (!attr) {
-    MSY_CK(cudaFuncSetAttribute(chase_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
-    attr = true;
-  }
-  SweepCtx* sc = sweep_ctx();
+  MSY_SMEM_ATTR_ONCE(chase_kernel<S>, smem_max);
   const int span = hi - lo;
   const long Tn = 4L * (nb - 1) + span;
   auto Lf = [&](long t) {
@@ -127,11 +126,21 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
     chase_kernel<S><<<1, nthr, (size_t)(nw + 1) * (2 * nw + 1) * sizeof(S), st>>>(H, ldh, lo, hi, nb, shifts, w.ws, w.we,
                                                                             w.t0, w.t1, Zbuf + (k & 1) * ZMAX * ZMAX);
     MSY_LAUNCH_CK();
-    MSY_CK(cudaEventRecord(sc->evC, st));
+    if (sc->aux) MSY_CK(cudaEventRecord(sc->evC, st));
     return 0;
   };
   int rc = chase(0);
   if (rc) return rc;
+  if (sc->aux == nullptr) {  // serial lane (batched executor): one stream, one Z application per window
+    for (int k = 0; k < nwins; k++) {
+      const Win& w = wins[k];
+      rc = apply_z<S>(m, w.we - w.ws, Zbuf + (k & 1) * ZMAX * ZMAX, H, ldh, U, ldu, w.ws, st);
+      if (rc) return rc;
+      if (k + 1 < nwins && (rc = chase(k + 1))) return rc;
+      if (nwin) (*nwin)++;
+    }
+    return 0;
+  }
   for (int k = 0; k < nwins; k++) {
     const Win& w = wins[k];
     const int nw = w.we - w.ws;
@@ -157,7 +166,9 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
 
 // In place: A (m x m, lda) -> T; U (m x m, ldu) = Schur vectors.
 template <class S>
-int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_t st, SchurStats* stats) {
+int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_t st, SchurStats* stats,
+                 SweepCtx* sc = nullptr) {
+  if (!sc) sc = sweep_ctx();
   typedef typename tr<S>::R R;
   constexpr int NMIN = SmallCfg<S>::NMAX;
   SchurStats loc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -165,8 +176,8 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     int rc = schur_small_launch<S>(m, A, lda, U, ldu, SS_HESS | SS_WANTZ, nullptr, nullptr, w.dinfo, st);
     if (rc) return rc;
     int hinfo[2];
-    MSY_CK(cudaMemcpyAsync(hinfo, w.dinfo, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
-    MSY_CK(cudaStreamSynchronize(st));
+    MSY_CK(d2h(hinfo, w.dinfo, sizeof(hinfo), st));
+    MSY_CK(host_sync(st));
     loc.status = hinfo[0];
     loc.sweeps = hinfo[1];
     loc.small_calls = 1;
@@ -183,8 +194,8 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     scan_kernel<S><<<1, 1024, 0, st>>>(m, A, lda, U, ldu, hi, w.dinfo);
     MSY_LAUNCH_CK();
     int hinfo[4];
-    MSY_CK(cudaMemcpyAsync(hinfo, w.dinfo, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    MSY_CK(cudaStreamSynchronize(st));
+    MSY_CK(d2h(hinfo, w.dinfo, 2 * sizeof(int), st));
+    MSY_CK(host_sync(st));
     hi = hinfo[0];
     int lo = hinfo[1];
     pt.lap(&loc.ms_scan);
@@ -198,8 +209,8 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
       rc = apply_z<S>(m, sz, w.Z, A, lda, U, ldu, lo, st);
       if (rc) return rc;
       int sinfo[2];
-      MSY_CK(cudaMemcpyAsync(sinfo, w.dinfo + 8, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-      MSY_CK(cudaStreamSynchronize(st));
+      MSY_CK(d2h(sinfo, w.dinfo + 8, 2 * sizeof(int), st));
+      MSY_CK(host_sync(st));
       pt.lap(&loc.ms_small);
       loc.small_calls++;
       loc.sweeps += sinfo[1];
@@ -224,7 +235,7 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     pair_shifts_kernel<S><<<1, 32, 0, st>>>(ns, w.wr, w.wi, nb, w.shifts, exc ? 1 : 0, A, lda, lo, hi, w.dinfo + 24);
     MSY_LAUNCH_CK();
     pt.lap(&loc.ms_shift);
-    rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, w.shifts, w.Z, st, &loc.windows);
+    rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, w.shifts, w.Z, st, &loc.windows, sc);
     if (rc) return rc;
     pt.lap(&loc.ms_sweep);
     loc.sweeps++;

@@ -1,0 +1,386 @@
+// schur_mss.cuh -- one-CTA small-bulge multishift QR for blocks held in shared memory.
+//
+// Same contract as schur_small_kernel (replaces `_hessenberg` + `schur`,
+// pkg/src/mpsylv/linalg.py:446-577, for blocks of order n <= SmallCfg<S>::NMAX),
+// but each QR sweep chases a chain of nb double-shift bulges (one warp per bulge,
+// bulges 4 rows apart, all bulges of a step in parallel, as in chase_kernel)
+// through the whole active block instead of one bulge at a time.  A sweep over
+// an active block of order s therefore costs ~s + 4 nb CTA steps for 2 nb
+// shifts, where the single-bulge kernel needs ~s steps per 2 shifts.
+//   * shifts: eigenvalues of the trailing 2nb x 2nb block, computed by warp 0
+//     with a warp-synchronous double-shift QR (warp_eig); nb = 1 uses the
+//     trailing 2x2 block (Francis double shift, as the single-bulge kernel);
+//   * deflation test and exceptional shifts follow the reference
+//     (linalg.py:541-557): |h_k,k-1| <= u (|h_k-1,k-1| + |h_kk|), exceptional
+//     shifts after stagnant sweeps, 30 n sweep limit;
+//   * real arithmetic keeps 2x2 blocks; complex arithmetic splits them with
+//     the eigenvector rotation so T is triangular (like the reference).
+#pragma once
+#include "common.cuh"
+#include "schur_small.cuh"
+
+namespace msy {
+
+template <class S> struct MssCfg { static constexpr int NWARP = 8; };
+constexpr int MSS_A2 = 33;  // ld of the shift-block scratch (<= 32 x 32 plus dummy row/column)
+
+// Eigenvalues of the k x k upper Hessenberg matrix A (smem, column-major, ld,
+// k <= 32; row/column `k` are dummies) by one warp; A is destroyed.
+// Returns ST_OK or ST_ITERLIMIT.
+template <class S>
+__device__ int warp_eig(int k, S* A, int ld, typename tr<S>::R* wr, typename tr<S>::R* wi, int lane) {
+  typedef typename tr<S>::R R;
+  const R u = tr<S>::u();
+#define AA(i, j) A[(i) + (j) * ld]
+  int i = k - 1, its = 0, total = 0;
+  while (i >= 0) {
+    const int kk = i - lane;
+    bool neg = false;
+    if (kk >= 1) {
+      S h = AA(kk, kk - 1);
+      neg = iszero(h) || absv(h) <= u * (absv(AA(kk - 1, kk - 1)) + absv(AA(kk, kk)));
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, neg);
+    const int l = mask ? i - (__ffs(mask) - 1) : 0;
+    __syncwarp();
+    if (l > 0 && lane == 0) AA(l, l - 1) = S(0);
+    if (l == i) {
+      if (lane == 0) { wr[i] = re(AA(i, i)); wi[i] = im(AA(i, i)); }
+      i -= 1; its = 0;
+      __syncwarp();
+      continue;
+    }
+    if (l == i - 1) {
+      R w4[4];
+      eig2<S>(AA(i - 1, i - 1), AA(i - 1, i), AA(i, i - 1), AA(i, i), w4);
+      if (lane == 0) { wr[i - 1] = w4[0]; wi[i - 1] = w4[1]; wr[i] = w4[2]; wi[i] = w4[3]; }
+      i -= 2; its = 0;
+      __syncwarp();
+      continue;
+    }
+    if (total >= 30 * k) return ST_ITERLIMIT;
+    its++; total++;
+    R w4[4];
+    if (its % 10 == 0) {
+      R s = absv(AA(i, i - 1)) + absv(AA(i - 1, i - 2));
+      S h11 = mk<S>(R(0.75) * s) + AA(i, i);
+      eig2<S>(h11, mk<S>(R(-0.4375) * s), mk<S>(s), h11, w4);
+    } else {
+      eig2<S>(AA(i - 1, i - 1), AA(i - 1, i), AA(i, i - 1), AA(i, i), w4);
+      if (!tr<S>::cx && w4[1] == R(0)) {
+        R hii = re(AA(i, i));
+        R s0 = fabs(w4[0] - hii) <= fabs(w4[2] - hii) ? w4[0] : w4[2];
+        w4[0] = w4[2] = s0;
+      }
+    }
+    for (int p = l - 1; p <= i - 2; p++) {
+      const int nr = (i - p) >= 3 ? 3 : 2;
+      S x0, x1, x2, beta, tau, v1, v2;
+      if (p < l) shift_poly<S>(AA(l, l), AA(l + 1, l), AA(l, l + 1), AA(l + 1, l + 1), AA(l + 2, l + 1), w4, x0, x1, x2);
+      else { x0 = AA(p + 1, p); x1 = AA(p + 2, p); x2 = nr > 2 ? AA(p + 3, p) : S(0); }
+      refl3_fast(nr, x0, x1, x2, beta, tau, v1, v2);
+      __syncwarp();
+      if (!iszero(tau)) {
+        const int rmax = (p + 4 < i) ? p + 4 : i;
+        if (nr == 3) {
+          warp_left3<S>(A, ld, p + 1, p + 1, i, k, conj(tau), v1, v2, lane);
+          __syncwarp();
+          warp_right3<S>(A, ld, p + 1, l, rmax, k, tau, v1, v2, lane);
+        } else {
+          const S ctau = conj(tau);
+          for (int c = p + 1 + lane; c <= i; c += 32) {
+            S h0 = AA(p + 1, c), h1 = AA(p + 2, c);
+            S w = ctau * fmacc(v1, h1, h0);
+            AA(p + 1, c) = h0 - w;
+            AA(p + 2, c) = h1 - v1 * w;
+          }
+          __syncwarp();
+          for (int r = l + lane; r <= rmax; r += 32) {
+            S a0 = AA(r, p + 1), a1 = AA(r, p + 2);
+            S w = tau * fmac(a1, v1, a0);
+            AA(r, p + 1) = a0 - w;
+            AA(r, p + 2) = a1 - w * conj(v1);
+          }
+        }
+      }
+      __syncwarp();
+      if (p >= l && lane == 0) {
+        AA(p + 1, p) = beta;
+        AA(p + 2, p) = S(0);
+        if (nr > 2) AA(p + 3, p) = S(0);
+      }
+      __syncwarp();
+    }
+  }
+#undef AA
+  return ST_OK;
+}
+
+// Pair ns eigenvalues (wr, wi) into nb bulge shift quadruples (sr1, si1, sr2, si2):
+// conjugate pairs stay together, real shifts are paired in order.  Returns the
+// number of distinct quadruples written (the rest repeat them).
+template <class S>
+__device__ int pair_shifts(int ns, const typename tr<S>::R* wr, const typename tr<S>::R* wi, int nb,
+                           typename tr<S>::R* out, typename tr<S>::R fallback_re, typename tr<S>::R fallback_im) {
+  typedef typename tr<S>::R R;
+  int b = 0;
+  if (tr<S>::cx) {
+    for (int k = 0; k + 1 < ns && b < nb; k += 2) {
+      out[4 * b] = wr[k]; out[4 * b + 1] = wi[k]; out[4 * b + 2] = wr[k + 1]; out[4 * b + 3] = wi[k + 1];
+      b++;
+    }
+  } else {
+    int pend = -1;
+    for (int k = 0; k < ns && b < nb; k++) {
+      if (wi[k] != R(0)) {
+        if (k + 1 < ns) {
+          out[4 * b] = wr[k]; out[4 * b + 1] = wi[k]; out[4 * b + 2] = wr[k + 1]; out[4 * b + 3] = wi[k + 1];
+          b++;
+        }
+        k++;
+        continue;
+      }
+      if (pend < 0) { pend = k; continue; }
+      out[4 * b] = wr[pend]; out[4 * b + 1] = 0; out[4 * b + 2] = wr[k]; out[4 * b + 3] = 0;
+      b++;
+      pend = -1;
+    }
+  }
+  if (b == 0) {
+    out[0] = fallback_re; out[1] = fallback_im; out[2] = fallback_re; out[3] = fallback_im;
+    b = 1;
+  }
+  for (int k = b; k < nb; k++)
+    for (int q = 0; q < 4; q++) out[4 * k + q] = out[4 * (k % b) + q];
+  return b;
+}
+
+template <class S>
+struct MssShared {
+  int l, status;
+  S bt[2];
+};
+
+template <class S>
+__global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S* Zg, int ldz, int flags,
+                                                       typename tr<S>::R* wr, typename tr<S>::R* wi, int* info) {
+  typedef typename tr<S>::R R;
+  constexpr int NW = MssCfg<S>::NWARP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ld = n + 1;
+  const bool wantz = flags & SS_WANTZ;
+  const bool eigonly = flags & SS_EIGONLY;
+  S* H = (S*)smem_raw;                        // n rows (+ dummy row n) x (n + 1) columns (dummy column n)
+  S* Zs = H + (size_t)ld * (n + 1);           // ld x n when wantz
+  S* A2 = Zs + (wantz ? (size_t)ld * n : 0);  // shift block scratch, MSS_A2 x MSS_A2
+  __shared__ MssShared<S> sh;
+  __shared__ S vbuf[SmallCfg<S>::NMAX + 4];
+  __shared__ R sw[4 * NW];                    // bulge shift quadruples
+  __shared__ R ewr[2 * NW + 2], ewi[2 * NW + 2];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const R u = tr<S>::u();
+#define HH(i, j) H[(i) + (j) * ld]
+#define ZZ(i, j) Zs[(i) + (j) * ld]
+  for (int e = tid; e < n * n; e += nt) {
+    int i = e % n, j = e / n;
+    HH(i, j) = Hg[i + (size_t)j * ldh];
+    if (wantz) ZZ(i, j) = (flags & SS_ZIN) ? Zg[i + (size_t)j * ldz] : (i == j ? S(1) : S(0));
+  }
+  __syncthreads();
+  if (flags & SS_HESS) smem_hessenberg<S>(n, H, Zs, ld, wantz, vbuf, sh.bt);
+
+  int i = n - 1, its = 0, total = 0, status = ST_OK;
+  while (i >= 0) {
+    // ---- deflation search (warp 0), broadcast through smem ----
+    if (warp == 0) {
+      int l = 0;
+      for (int base = i; base >= 1; base -= 32) {
+        const int k = base - lane;
+        bool neg = false;
+        if (k >= 1) {
+          S h = HH(k, k - 1);
+          neg = iszero(h) || absv(h) <= u * (absv(HH(k - 1, k - 1)) + absv(HH(k, k)));
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, neg);
+        if (mask) { l = base - (__ffs(mask) - 1); break; }
+      }
+      if (lane == 0) {
+        sh.l = l;
+        if (l > 0) HH(l, l - 1) = S(0);
+      }
+    }
+    __syncthreads();
+    const int l = sh.l;
+    if (l == i) {
+      if (wr && tid == 0) { wr[i] = re(HH(i, i)); wi[i] = im(HH(i, i)); }
+      i -= 1; its = 0;
+      __syncthreads();  // sh.l is rewritten by the next search
+      continue;
+    }
+    if (l == i - 1) {
+      R w4[4];
+      eig2<S>(HH(i - 1, i - 1), HH(i - 1, i), HH(i, i - 1), HH(i, i), w4);
+      if (wr && tid == 0) { wr[i - 1] = w4[0]; wi[i - 1] = w4[1]; wr[i] = w4[2]; wi[i] = w4[3]; }
+      if (tr<S>::cx) {  // split with the eigenvector rotation (first column g = v / |v|)
+        S a = HH(l, l), b = HH(l, i), c = HH(i, l), d = HH(i, i);
+        S lam = mk<S>(w4[0], w4[1]);
+        S va = lam - d, vb = c, wa = b, wb = lam - a;
+        if (abs2(wa) + abs2(wb) > abs2(va) + abs2(vb)) { va = wa; vb = wb; }
+        R nv = sqrt(abs2(va) + abs2(vb));
+        S g11 = va / mk<S>(nv), g21 = vb / mk<S>(nv);
+        S g12 = -conj(g21), g22 = conj(g11);
+        __syncthreads();
+        const int jmax = eigonly ? i : n - 1;
+        for (int j = l + tid; j <= jmax; j += nt) {
+          S h1 = HH(l, j), h2 = HH(i, j);
+          HH(l, j) = fmacc(g11, h1, conj(g21) * h2);
+          HH(i, j) = fmacc(g12, h1, conj(g22) * h2);
+        }
+        __syncthreads();
+        const int rmin = eigonly ? l : 0;
+        for (int r = rmin + tid; r <= i; r += nt) {
+          S c1 = HH(r, l), c2 = HH(r, i);
+          HH(r, l) = c1 * g11 + c2 * g21;
+          HH(r, i) = c1 * g12 + c2 * g22;
+        }
+        if (wantz)
+          for (int r = tid; r < n; r += nt) {
+            S c1 = ZZ(r, l), c2 = ZZ(r, i);
+            ZZ(r, l) = c1 * g11 + c2 * g21;
+            ZZ(r, i) = c1 * g12 + c2 * g22;
+          }
+        __syncthreads();
+        if (tid == 0) HH(i, l) = S(0);
+      }
+      __syncthreads();
+      i -= 2; its = 0;
+      continue;
+    }
+    if (total >= 30 * n) { status = ST_ITERLIMIT; break; }
+    its++; total++;
+    const int sz = i - l + 1;
+    const int nb = min(NW, max(1, sz / 10));
+    const int ns = 2 * nb;
+    // ---- shifts (warp 0) ----
+    if (warp == 0) {
+      const bool exc = (its % 6 == 0);
+      if (nb == 1 || exc) {
+        for (int b = 0; b < nb; b++) {
+          R w4[4];
+          if (exc) {
+            int ii = i - 2 * b;
+            if (ii - 2 < l) ii = i;
+            R s = absv(HH(ii, ii - 1)) + absv(HH(ii - 1, ii - 2));
+            S h11 = mk<S>(R(0.75) * s) + HH(ii, ii);
+            eig2<S>(h11, mk<S>(R(-0.4375) * s), mk<S>(s), h11, w4);
+          } else {
+            eig2<S>(HH(i - 1, i - 1), HH(i - 1, i), HH(i, i - 1), HH(i, i), w4);
+            if (!tr<S>::cx && w4[1] == R(0)) {
+              R hii = re(HH(i, i));
+              R s0 = fabs(w4[0] - hii) <= fabs(w4[2] - hii) ? w4[0] : w4[2];
+              w4[0] = w4[2] = s0;
+            }
+          }
+          if (lane == 0)
+            for (int q = 0; q < 4; q++) sw[4 * b + q] = w4[q];
+        }
+      } else {
+        const int k0 = i - ns + 1;
+        for (int e = lane; e < ns * ns; e += 32) {
+          int r = e % ns, c = e / ns;
+          A2[r + c * MSS_A2] = (r <= c + 1) ? HH(k0 + r, k0 + c) : S(0);
+        }
+        __syncwarp();
+        int st = warp_eig<S>(ns, A2, MSS_A2, ewr, ewi, lane);
+        __syncwarp();
+        if (lane == 0) {
+          if (st != ST_OK) {  // fall back to the trailing diagonal entry
+            for (int q = 0; q < ns; q++) { ewr[q] = re(HH(i, i)); ewi[q] = im(HH(i, i)); }
+          }
+          pair_shifts<S>(ns, ewr, ewi, nb, sw, re(HH(i, i)), im(HH(i, i)));
+        }
+      }
+    }
+    __syncthreads();
+    // ---- sweep: nb bulges, one warp each, 4 rows apart ----
+    const int jmax = eigonly ? i : n - 1;  // last column of left ops
+    const int rmin = eigonly ? l : 0;      // first row of right ops
+    const int T = (i - l) + 4 * (nb - 1);
+    const int j = warp;
+    for (int t = 0; t < T; t++) {
+      const int p = l - 1 + t - 4 * j;
+      const bool act = (j < nb) && (p >= l - 1) && (p <= i - 2);
+      const int nr = (i - p) >= 3 ? 3 : 2;
+      S tau = S(0), v1 = S(0), v2 = S(0);
+      if (act) {
+        S x0, x1, x2, beta;
+        if (p == l - 1) {
+          shift_poly<S>(HH(l, l), HH(l + 1, l), HH(l, l + 1), HH(l + 1, l + 1), (l + 2 <= i) ? HH(l + 2, l + 1) : S(0),
+                        sw + 4 * j, x0, x1, x2);
+        } else {
+          x0 = HH(p + 1, p); x1 = HH(p + 2, p); x2 = nr > 2 ? HH(p + 3, p) : S(0);
+        }
+        refl3_fast(nr, x0, x1, x2, beta, tau, v1, v2);
+        __syncwarp();
+        if (!iszero(tau)) {
+          if (nr == 3) {
+            warp_left3<S>(H, ld, p + 1, p + 1, jmax, n, conj(tau), v1, v2, lane);
+          } else {
+            const S ctau = conj(tau);
+            for (int c = p + 1 + lane; c <= jmax; c += 32) {
+              S h0 = HH(p + 1, c), h1 = HH(p + 2, c);
+              S w = ctau * fmacc(v1, h1, h0);
+              HH(p + 1, c) = h0 - w;
+              HH(p + 2, c) = h1 - v1 * w;
+            }
+          }
+        }
+        if (p >= l && lane == 0) {
+          HH(p + 1, p) = beta;
+          HH(p + 2, p) = S(0);
+          if (nr > 2) HH(p + 3, p) = S(0);
+        }
+      }
+      __syncthreads();
+      if (act && !iszero(tau)) {
+        const int rmax = (p + 4 < i) ? p + 4 : i;
+        if (nr == 3) {
+          warp_right3<S>(H, ld, p + 1, rmin, rmax, n, tau, v1, v2, lane);
+          if (wantz) warp_right3<S>(Zs, ld, p + 1, 0, n - 1, n, tau, v1, v2, lane);
+        } else {
+          for (int pass = 0; pass < (wantz ? 2 : 1); pass++) {
+            S* M = pass == 0 ? H : Zs;
+            const int r0 = pass == 0 ? rmin : 0, r1 = pass == 0 ? rmax : n - 1;
+            for (int r = r0 + lane; r <= r1; r += 32) {
+              S a0 = M[r + (p + 1) * ld], a1 = M[r + (p + 2) * ld];
+              S w = tau * fmac(a1, v1, a0);
+              M[r + (p + 1) * ld] = a0 - w;
+              M[r + (p + 2) * ld] = a1 - w * conj(v1);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) { sh.status = status; }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += nt) {
+    int r = e % n, c = e / n;
+    Hg[r + (size_t)c * ldh] = HH(r, c);
+    if (wantz) Zg[r + (size_t)c * ldz] = ZZ(r, c);
+  }
+  if (tid == 0 && info) {
+    info[0] = sh.status;
+    info[1] = total;
+  }
+#undef HH
+#undef ZZ
+}
+
+template <class S>
+static size_t mss_smem_bytes(int n, bool wantz) {
+  return ((size_t)(n + 1) * (n + 1) + (wantz ? (size_t)(n + 1) * n : 0) + (size_t)MSS_A2 * MSS_A2) * sizeof(S) + 64;
+}
+
+}  // namespace msy

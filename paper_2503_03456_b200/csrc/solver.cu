@@ -17,7 +17,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -34,6 +38,8 @@ using namespace msy;
 namespace {
 
 struct StreamCtx {
+  SweepCtx swA, swB;  // aux streams of the two concurrent Schur factorisations
+  SweepCtx serial;    // no aux stream: batched lanes run everything on their own stream
   cudaStream_t side = nullptr;
   cudaEvent_t ev_in = nullptr, ev_side = nullptr;
   cudaEvent_t ev[8];
@@ -41,6 +47,8 @@ struct StreamCtx {
   int device = -1;
 };
 thread_local StreamCtx g_ctx;
+// batched lanes: one stream per lane, Schur(A) then Schur(B) (concurrency comes from the lanes)
+thread_local bool t_serial_lane = false;
 
 int ctx_init() {
   int dev;
@@ -50,6 +58,8 @@ int ctx_init() {
   MSY_CK(cudaEventCreateWithFlags(&g_ctx.ev_in, cudaEventDisableTiming));
   MSY_CK(cudaEventCreateWithFlags(&g_ctx.ev_side, cudaEventDisableTiming));
   for (int i = 0; i < 8; i++) MSY_CK(cudaEventCreate(&g_ctx.ev[i]));
+  g_ctx.swA.ensure();
+  g_ctx.swB.ensure();
   g_ctx.init = true;
   g_ctx.device = dev;
   return 0;
@@ -118,16 +128,16 @@ int read_reduce(S* X, int rows, int cols, int ld, const S* Yv, int ldy, int mode
                 double out[3], cudaStream_t st) {
   int rc = reduce<S>(mode, rows, cols, X, ld, Yv, ldy, part, red, st);
   if (rc) return rc;
-  MSY_CK(cudaMemcpyAsync(out, red, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  MSY_CK(cudaStreamSynchronize(st));
+  MSY_CK(d2h(out, red, 3 * sizeof(double), st));
+  MSY_CK(host_sync(st));
   return 0;
 }
 
 // decode the trsyl status word into (status, row, col)
 int read_trsyl_status(int* dstat, int m, int n, int lowerB, int* row, int* col, cudaStream_t st) {
   int h[4];
-  MSY_CK(cudaMemcpyAsync(h, dstat, sizeof(h), cudaMemcpyDeviceToHost, st));
-  MSY_CK(cudaStreamSynchronize(st));
+  MSY_CK(d2h(h, dstat, sizeof(h), st));
+  MSY_CK(host_sync(st));
   if (h[0] == 0x7fffffff) return SYLV_OK;
   int crank = h[0] / m, i = m - 1 - h[0] % m;
   *row = i;
@@ -208,13 +218,20 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
                    cudaStream_t st, int* ovf, SchurStats* sa, SchurStats* sb) {
   int rc = convert<Ll, Hh>(m, m, A, lda, w.TA, m, ovf, st);
   if (rc) return rc;
+  SweepCtx* sca = t_serial_lane ? &g_ctx.serial : &g_ctx.swA;
   if (kind == SYLV_KIND_LYAPUNOV) {
-    rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, st, sa);
+    rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, st, sa, sca);
     if (rc) return rc;
     rc = conj_transpose<Ll>(m, m, w.TA, m, w.TB, n, st);
     if (rc) return rc;
     rc = copy2d<Ll>(m, m, w.UA, m, w.UB, n, st);
     *sb = *sa;
+    return rc;
+  }
+  if (t_serial_lane) {
+    rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, st, sa, sca);
+    if (!rc) rc = convert<Ll, Hh>(n, n, B, ldb, w.TB, n, ovf + 1, st);
+    if (!rc) rc = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, st, sb, sca);
     return rc;
   }
   MSY_CK(cudaEventRecord(g_ctx.ev_in, st));
@@ -224,12 +241,15 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
   int rcb = 0;
   cudaStream_t side = g_ctx.side;
   int* ovf_b = ovf + 1;
+  SweepCtx* scb = &g_ctx.swB;
+  const bool blocking = host_sync_blocking();
   std::thread tb([&]() {
     cudaSetDevice(dev);
+    host_sync_blocking() = blocking;
     rcb = convert<Ll, Hh>(n, n, B, ldb, w.TB, n, ovf_b, side);
-    if (!rcb) rcb = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, side, sb);
+    if (!rcb) rcb = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, side, sb, scb);
   });
-  rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, st, sa);
+  rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, st, sa, &g_ctx.swA);
   tb.join();
   if (rc) return rc;
   if (rcb) return rcb;
@@ -264,8 +284,8 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
   rep->schur_sweeps_a = sa.sweeps;
   rep->schur_sweeps_b = sb.sweeps;
   int hovf[2];
-  MSY_CK(cudaMemcpyAsync(hovf, ovf, sizeof(hovf), cudaMemcpyDeviceToHost, st));
-  MSY_CK(cudaStreamSynchronize(st));
+  MSY_CK(d2h(hovf, ovf, sizeof(hovf), st));
+  MSY_CK(host_sync(st));
   if (hovf[0] || hovf[1]) { rep->status = SYLV_FORMAT_OVERFLOW; return 0; }
   if (sa.status || sb.status) { rep->status = SYLV_ITERATION_LIMIT; return 0; }
   tm.mark();  // 1
@@ -284,9 +304,9 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
     if (rc) return rc;
     int hflag;
     double hdiag;
-    MSY_CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    MSY_CK(cudaMemcpyAsync(&hdiag, ddiag, sizeof(double), cudaMemcpyDeviceToHost, st));
-    MSY_CK(cudaStreamSynchronize(st));
+    MSY_CK(d2h(&hflag, dflag, sizeof(int), st));
+    MSY_CK(d2h(&hdiag, ddiag, sizeof(double), st));
+    MSY_CK(host_sync(st));
     // _check_rank (linalg.py:244-249): min R_jj <= n u ||U||_F
     if (hflag || hdiag <= m * tr<Hh>::u() * std::sqrt(o[0])) { rep->status = SYLV_RANK_DEFICIENT; return 0; }
     if (lyap) {
@@ -300,9 +320,9 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
       if (rc) return rc;
       rc = read_reduce<Hh>(w.TBh, n, n, n, nullptr, 0, 0, w.part, w.red, o, st);
       if (rc) return rc;
-      MSY_CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-      MSY_CK(cudaMemcpyAsync(&hdiag, ddiag, sizeof(double), cudaMemcpyDeviceToHost, st));
-      MSY_CK(cudaStreamSynchronize(st));
+      MSY_CK(d2h(&hflag, dflag, sizeof(int), st));
+      MSY_CK(d2h(&hdiag, ddiag, sizeof(double), st));
+      MSY_CK(host_sync(st));
       if (hflag || hdiag <= n * tr<Hh>::u() * std::sqrt(o[0])) { rep->status = SYLV_RANK_DEFICIENT; return 0; }
     }
     if (rc) return rc;
@@ -390,7 +410,7 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
       rep->iterations = 0;
       rep->residual = NAN;
       fill<Hh>(m, n, mk<Hh>(NAN, NAN), X, ldx, st);
-      MSY_CK(cudaStreamSynchronize(st));
+      MSY_CK(host_sync(st));
       return 0;
     }
     fill<Hh>(m, n, Hh(0), w.Y, m, st);
@@ -410,7 +430,7 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
     rep->converged = 0;
     rep->residual = NAN;
     fill<Hh>(m, n, mk<Hh>(NAN, NAN), X, ldx, st);
-    MSY_CK(cudaStreamSynchronize(st));
+    MSY_CK(host_sync(st));
     return 0;
   }
   tm.mark();  // 5
@@ -448,7 +468,7 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
   rep->backward_error = (a + b) * x == 0.0 ? 0.0 : num / ((a + b) * x);
   rep->norm_x = x;
   tm.mark();  // 7
-  MSY_CK(cudaStreamSynchronize(st));
+  MSY_CK(host_sync(st));
   rep->ms_schur = tm.ms(0, 1);
   rep->ms_orth = tm.ms(1, 2);
   rep->ms_setup = tm.ms(2, 3);
@@ -535,6 +555,131 @@ int sylv_solve(const sylv_params* p, const void* A, int lda, const void* B, int 
                                        (cdouble*)X, ldx, ws, ws_bytes, st, rep);
   return solve_impl<cdouble, cdouble>(p, (const cdouble*)A, lda, (const cdouble*)B, ldb, (const cdouble*)C, ldc,
                                       (cdouble*)X, ldx, ws, ws_bytes, st, rep);
+}
+
+// ---- batched executor (C4) ---------------------------------------------------
+// A persistent pool of host worker threads ("lanes").  Each lane owns a stream,
+// its thread-local solve context (side / aux streams, events) and a slice of the
+// caller's workspace; lanes pull equation indices from a shared counter and run
+// the ordinary single-equation driver with blocking-sync host waits.
+namespace {
+
+class LanePool {
+ public:
+  static LanePool& get() {
+    static LanePool* p = new LanePool;  // leaked on purpose: workers outlive static destruction
+    return *p;
+  }
+  // run fn(lane) on lanes 0..n-1 concurrently; returns when all have finished
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> call(call_mu_);
+    std::unique_lock<std::mutex> g(mu_);
+    while ((int)th_.size() < n) {
+      int id = (int)th_.size();
+      th_.emplace_back([this, id] { loop(id); });
+    }
+    fn_ = &fn;
+    nrun_ = n;
+    pending_ = n;
+    gen_++;
+    cv_.notify_all();
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(int id) {
+    int seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (id >= nrun_) continue;
+        f = fn_;
+      }
+      (*f)(id);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> th_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int nrun_ = 0, pending_ = 0, gen_ = 0;
+};
+
+struct LaneStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t done = nullptr;
+  int dev = -1;
+};
+
+constexpr int kDefaultLanes = 32;
+
+int lanes_for(int lanes, int batch) { return std::max(1, std::min(lanes > 0 ? lanes : kDefaultLanes, batch)); }
+
+}  // namespace
+
+int sylv_batched_workspace_size(const sylv_params* p, int lanes, size_t* bytes) {
+  if (!bytes) return SYLV_EINVAL;
+  size_t one = 0;
+  int rc = sylv_workspace_size(p, &one);
+  if (rc) return rc;
+  one = (one + 255) & ~(size_t)255;
+  *bytes = one * (size_t)(lanes > 0 ? lanes : kDefaultLanes);
+  return 0;
+}
+
+int sylv_solve_batched(const sylv_params* p, int batch, const void* const* A, int lda, const void* const* B, int ldb,
+                       const void* const* C, int ldc, void* const* X, int ldx, int lanes, void* ws, size_t ws_bytes,
+                       void* stream, sylv_report* reports) {
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (batch < 0 || (batch > 0 && (!A || !B || !C || !X || !reports))) return SYLV_EINVAL;
+  if (batch == 0) return 0;
+  const int nl = lanes_for(lanes, batch);
+  size_t one = 0;
+  rc = sylv_workspace_size(p, &one);
+  if (rc) return rc;
+  one = (one + 255) & ~(size_t)255;
+  if (!ws || ws_bytes < one * (size_t)nl) return SYLV_EWORKSPACE;
+  int dev;
+  MSY_CK(cudaGetDevice(&dev));
+  cudaStream_t cst = (cudaStream_t)stream;
+  cudaEvent_t start;
+  MSY_CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  MSY_CK(cudaEventRecord(start, cst));
+  std::atomic<int> next{0}, err{0};
+  std::vector<cudaEvent_t> done(nl, nullptr);
+  std::function<void(int)> fn = [&](int lane) {
+    thread_local LaneStream ls;
+    if (cudaSetDevice(dev) != cudaSuccess) { err.store(SYLV_ECUDA); return; }
+    if (ls.st == nullptr || ls.dev != dev) {
+      cudaStreamCreateWithFlags(&ls.st, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&ls.done, cudaEventDisableTiming);
+      ls.dev = dev;
+    }
+    host_sync_blocking() = true;
+    t_serial_lane = true;
+    cudaStreamWaitEvent(ls.st, start, 0);
+    char* mine = (char*)ws + one * (size_t)lane;
+    for (int i; (i = next.fetch_add(1)) < batch && err.load() == 0;) {
+      int r = sylv_solve(p, A[i], lda, B[i], ldb, C[i], ldc, X[i], ldx, mine, one, ls.st, &reports[i]);
+      if (r) { int z = 0; err.compare_exchange_strong(z, r); }
+    }
+    cudaEventRecord(ls.done, ls.st);
+    done[lane] = ls.done;
+    host_sync_blocking() = false;
+    t_serial_lane = false;
+  };
+  LanePool::get().run(nl, fn);
+  for (int l = 0; l < nl; l++)
+    if (done[l]) MSY_CK(cudaStreamWaitEvent(cst, done[l], 0));
+  cudaEventDestroy(start);
+  return err.load();
 }
 
 // ---- solve_pert_sylv_tri_stat --------------------------------------------
@@ -650,7 +795,7 @@ static int schur_entry(int m, void* A, int lda, void* U, int ldu, void* ws, size
   SchurStats s{};
   int rc = schur_device<S>(m, (S*)A, lda, (S*)U, ldu, w, st, &s);
   if (rc) return rc;
-  MSY_CK(cudaStreamSynchronize(st));
+  MSY_CK(host_sync(st));
   if (info) { info[0] = s.status; info[1] = s.sweeps; info[2] = s.small_calls; info[3] = s.windows; }
   if (getenv("MSY_SCHUR_TIMING"))
     fprintf(stderr, "schur m=%d: hess %.1f ms, scan %.1f, small %.1f, shift %.1f, sweep %.1f\n", m, s.ms_hess,
@@ -739,9 +884,9 @@ static int orth_entry(int m, const void* U, int ldu, void* Q, int ldq, void* R, 
   if (rc) return rc;
   int hflag;
   double hdiag;
-  MSY_CK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  MSY_CK(cudaMemcpyAsync(&hdiag, red + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
-  MSY_CK(cudaStreamSynchronize(st));
+  MSY_CK(d2h(&hflag, flag, sizeof(int), st));
+  MSY_CK(d2h(&hdiag, red + 8, sizeof(double), st));
+  MSY_CK(host_sync(st));
   if (info) info[0] = (hflag || hdiag <= m * tr<S>::u() * std::sqrt(o[0])) ? SYLV_RANK_DEFICIENT : SYLV_OK;
   return 0;
 }

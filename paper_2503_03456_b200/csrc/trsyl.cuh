@@ -392,12 +392,7 @@ template <class S>
 int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, S* W, int ldw, TrsylWs<S>& w,
           int* status, cudaStream_t st) {
   constexpr int NB = TrsylCfg<S>::NB;
-  static bool attr = false;
-  if (!attr) {
-    MSY_CK(cudaFuncSetAttribute(trsyl_step_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)trsyl_smem<S>()));
-    attr = true;
-  }
+  MSY_SMEM_ATTR_ONCE(trsyl_step_kernel<S>, (int)trsyl_smem<S>());
   const int nbi = cdiv(m, NB), nbj = cdiv(n, NB);
   trsyl_partition_kernel<S><<<cdiv(max(nbi, nbj) + 1, 128), 128, 0, st>>>(m, TA, lda, n, TB, ldb, lowerB, NB, w.rb,
                                                                           nbi, w.cb, nbj);

@@ -145,3 +145,40 @@ def test_stationary_refinement_matches_oracle(B200, oracle, golden_kernels):
     rep = B200.solve_pert_sylv_tri_stat(np.array([[1.0]]), np.array([[0.5]]), np.array([[-0.9]]),
                                         np.array([[0.0]]), np.array([[1.0]]), np.array([[0.0]]), cfg)
     assert not rep.converged and rep.correction_norms[-1] > rep.correction_norms[0]
+
+
+@pytest.mark.parametrize("variant", ["orth", "inv"])
+def test_batched_matches_single_solves(B200, variant):
+    """C4 path: the lane executor returns, equation by equation, exactly what the
+    single-equation driver returns (same kernels, deterministic reductions)."""
+    import torch
+    from paper_2503_03456_b200 import problems as P
+    nb, m = 6, 96
+    probs = [P.make_c4(i, m) for i in range(nb)]
+    A = torch.stack([torch.as_tensor(p.A) for p in probs]).cuda()
+    B = torch.stack([torch.as_tensor(p.B) for p in probs]).cuda()
+    C = torch.stack([torch.as_tensor(p.C) for p in probs]).cuda()
+    X, reps = B200.solve_batched(A, B, C, variant=variant, lanes=4)
+    assert len(reps) == nb
+    for i in range(nb):
+        Xi, ri = B200.solve(A[i], B[i], C[i], variant=variant)
+        assert reps[i].status == 0 and reps[i].iterations == ri.iterations == 2
+        assert torch.equal(X[i], Xi)
+        An, Bn, Cn = probs[i].A, probs[i].B, probs[i].C
+        assert backward(An, Bn, Cn, X[i].cpu().numpy()) < 1e-15
+
+
+def test_batched_c4_size_against_oracle(B200, oracle):
+    """Full-size C4 equations (m = n = 512) through the batched path; equation 0 vs the oracle's Alg. 3."""
+    import torch
+    from paper_2503_03456_b200 import problems as P
+    probs = [P.make_c4(i, 512) for i in range(2)]
+    A = torch.stack([torch.as_tensor(p.A) for p in probs]).cuda()
+    B = torch.stack([torch.as_tensor(p.B) for p in probs]).cuda()
+    C = torch.stack([torch.as_tensor(p.C) for p in probs]).cuda()
+    X, reps = B200.solve_batched(A, B, C, lanes=2)
+    for i, p in enumerate(probs[:1]):
+        ref = oracle.mp_solve(p.A, p.B, p.C, "orth", "binary32")
+        assert abs(reps[i].iterations - ref["iterations"]) <= 1
+        be_ref = backward(p.A, p.B, p.C, ref["X"].real)
+        assert backward(p.A, p.B, p.C, X[i].cpu().numpy()) <= 10 * max(be_ref, U64)
