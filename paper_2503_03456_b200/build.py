@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if not force and up_to_date():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES]
+    extra = os.environ.get("MSY_EXTRA_NVCC_FLAGS", "").split()  # developer A/B switches
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", *SOURCES]
     if verbose:
         print("[build]", " ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=HERE)

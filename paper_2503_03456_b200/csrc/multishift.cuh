@@ -35,16 +35,25 @@ constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
 // rows/columns; the two phases order the only overlapping entries.  The warp
 // ops are branch-free (warp_left3 / warp_right3 redirect idle lanes to a dummy
 // row/column of the smem window).
+constexpr int KMAX = 4;  // bulge chains in flight per sweep (one CTA each)
 template <class S>
-__global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int hi, int nb,
-                                                    const typename tr<S>::R* __restrict__ shifts, int ws, int we,
-                                                    int t0, int t1, S* Zg) {
+struct ChaseJobs {
+  int ws[KMAX], we[KMAX], t0[KMAX], t1[KMAX];
+  const typename tr<S>::R* shifts[KMAX];
+  S* Z[KMAX];
+};
+
+template <class S>
+__global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int hi, int nb, const ChaseJobs<S> jobs) {
   typedef typename tr<S>::R R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ws = jobs.ws[blockIdx.x], we = jobs.we[blockIdx.x], t0 = jobs.t0[blockIdx.x], t1 = jobs.t1[blockIdx.x];
+  const R* __restrict__ shifts = jobs.shifts[blockIdx.x];
+  S* Zg = jobs.Z[blockIdx.x];
   const int nw = we - ws;
-  const int ld = nw + 1;                // row nw of every column is the dummy row
-  S* Hw = (S*)smem_raw;                 // nw rows x (nw + 1) columns (column nw is the dummy)
-  S* Zw = Hw + (size_t)ld * (nw + 1);   // nw rows x nw columns
+  constexpr int ld = MsCfg<S>::W + 1;   // fixed stride: immediate smem offsets in the warp ops
+  S* Hw = (S*)smem_raw;                 // nw rows x nw columns (stride ld)
+  S* Zw = Hw + (size_t)ld * MsCfg<S>::W;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
 #define HW(i, j) Hw[(i) + (j) * ld]
 #define ZW(i, j) Zw[(i) + (j) * ld]
@@ -74,17 +83,8 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
       refl3_fast(nr, x0, x1, x2, beta, tau, v1, v2);
       __syncwarp();
       if (!iszero(tau)) {
-        if (nr == 3) {
-          warp_left3<S>(Hw, ld, pl + 1, pl + 1, nw - 1, nw, conj(tau), v1, v2, lane);
-        } else {
-          const S ctau = conj(tau);
-          for (int c = pl + 1 + lane; c < nw; c += 32) {
-            S h0 = HW(pl + 1, c), h1 = HW(pl + 2, c);
-            S w = ctau * fmacc(v1, h1, h0);
-            HW(pl + 1, c) = h0 - w;
-            HW(pl + 2, c) = h1 - v1 * w;
-          }
-        }
+        if (nr == 3) wl3<S, ld>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, v2, lane);
+        else wl2<S, ld>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, lane);
       }
       if (p >= lo && lane == 0) {
         HW(pl + 1, pl) = beta;
@@ -100,19 +100,11 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
       const int rmax = ((p + 4 < hi) ? p + 4 : hi) - ws;
       const int zmax = min(nw - 1, (lo - 1 + t) - ws + 3);
       if (nr == 3) {
-        warp_right3<S>(Hw, ld, pl + 1, 0, rmax, nw, tau, v1, v2, lane);
-        warp_right3<S>(Zw, ld, pl + 1, 0, zmax, nw, tau, v1, v2, lane);
+        wr3<S, ld>(Hw, pl + 1, 0, rmax, tau, v1, v2, lane);
+        wr3<S, ld>(Zw, pl + 1, 0, zmax, tau, v1, v2, lane);
       } else {
-        for (int pass = 0; pass < 2; pass++) {
-          S* M = pass == 0 ? Hw : Zw;
-          const int last = pass == 0 ? rmax : zmax;
-          for (int r = lane; r <= last; r += 32) {
-            S a0 = M[r + (pl + 1) * ld], a1 = M[r + (pl + 2) * ld];
-            S w = tau * fmac(a1, v1, a0);
-            M[r + (pl + 1) * ld] = a0 - w;
-            M[r + (pl + 2) * ld] = a1 - w * conj(v1);
-          }
-        }
+        wr2<S, ld>(Hw, pl + 1, 0, rmax, tau, v1, lane);
+        wr2<S, ld>(Zw, pl + 1, 0, zmax, tau, v1, lane);
       }
     }
     __syncthreads();
@@ -132,16 +124,16 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
 //   region R: H[0:rR1, r0:r0+nz]   <- (.) * Z          (tiles of 32 rows)
 //   region U: U[0:mU, r0:r0+nz]    <- (.) * Z
 template <class S>
-__global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restrict__ Zg, S* H, int ldh, int r0,
-                                                      int cL0, int cL1, int rR1, S* U, int ldu, int mU) {
+__device__ __forceinline__ void apply_z_block(int b, unsigned char* smem_raw, int nz, const S* __restrict__ Zg, S* H,
+                                              int ldh, int r0, int cL0, int cL1, int rlo, int rR1, S* U, int ldu,
+                                              int mU) {
   constexpr int ZA = ZMAX / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ldz = nz + 1;
   S* Zs = (S*)smem_raw;
   S* Ts = Zs + (size_t)ldz * nz;
   const int tid = threadIdx.x;
-  const int ntL = cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0, ntR = cdiv(rR1, 32), ntU = cdiv(mU, 32);
-  int b = blockIdx.x;
+  const int ntL = cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0, ntR = rR1 > rlo ? cdiv(rR1 - rlo, 32) : 0,
+            ntU = cdiv(mU, 32);
   for (int e = tid; e < nz * nz; e += 256) Zs[(e % nz) + (e / nz) * ldz] = Zg[e];
   if (b < ntL) {
     const int c0 = cL0 + b * 32, nc = min(32, cL1 - c0);
@@ -184,7 +176,7 @@ __global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restric
   b -= ntL;
   S* M;
   int ldm, rbase, nrows;
-  if (b < ntR) { M = H; ldm = ldh; rbase = b * 32; nrows = min(32, rR1 - rbase); }
+  if (b < ntR) { M = H; ldm = ldh; rbase = rlo + b * 32; nrows = min(32, rR1 - rbase); }
   else { b -= ntR; if (b >= ntU) return; M = U; ldm = ldu; rbase = b * 32; nrows = min(32, mU - rbase); }
   for (int e = tid; e < 32 * nz; e += 256) {
     int r = e % 32, c = e / 32;
@@ -219,6 +211,29 @@ __global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restric
       if (jj < nz) M[(rbase + r) + (size_t)(r0 + jj) * ldm] = acc[a][q];
     }
   }
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) apply_z_kernel(int nz, const S* __restrict__ Zg, S* H, int ldh, int r0,
+                                                      int cL0, int cL1, int rR1, S* U, int ldu, int mU) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  apply_z_block<S>(blockIdx.x, smem_raw, nz, Zg, H, ldh, r0, cL0, cL1, 0, rR1, U, ldu, mU);
+}
+
+// several windows' applications in one launch (disjoint regions; blocks [start[j], start[j+1]) -> job j)
+template <class S>
+struct ApplyJobs {
+  int n;
+  int start[KMAX + 1], nz[KMAX], r0[KMAX], cL0[KMAX], cL1[KMAX], rlo[KMAX], rR1[KMAX], mU[KMAX];
+  const S* Z[KMAX];
+};
+template <class S>
+__global__ void __launch_bounds__(256) apply_z_multi_kernel(S* H, int ldh, S* U, int ldu, const ApplyJobs<S> jobs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int j = 0;
+  while (j + 1 < jobs.n && (int)blockIdx.x >= jobs.start[j + 1]) j++;
+  apply_z_block<S>(blockIdx.x - jobs.start[j], smem_raw, jobs.nz[j], jobs.Z[j], H, ldh, jobs.r0[j], jobs.cL0[j],
+                   jobs.cL1[j], jobs.rlo[j], jobs.rR1[j], U, ldu, jobs.mU[j]);
 }
 
 template <class S>

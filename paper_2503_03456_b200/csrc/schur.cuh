@@ -30,11 +30,11 @@ struct SchurWs {
   int* dinfo; // small device ints
   static void carve(Arena& ar, int m, SchurWs& w) {
     if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
-    w.Z = ar.get<S>(2 * ZMAX * ZMAX);
+    w.Z = ar.get<S>((size_t)2 * KMAX * ZMAX * ZMAX);
     w.sblk = ar.get<S>(128 * 128);
     w.wr = ar.get<R>(256);
     w.wi = ar.get<R>(256);
-    w.shifts = ar.get<R>(4 * 64);
+    w.shifts = ar.get<R>(4 * 128);
     w.dinfo = ar.get<int>(64);
   }
 };
@@ -84,16 +84,27 @@ inline SweepCtx* sweep_ctx() {
   return &c;
 }
 
-// One multishift sweep over the active block [lo, hi] with nb bulges.
-// Windows are planned on the host (bulge positions are a function of the step).
-// Pipeline: chase(k+1) on `st` runs concurrently with the far part of apply(k)
-// on `aux`; the near part (columns the next window will load) runs first.
+// One multishift sweep over the active block [lo, hi]: K chains of nb bulges each
+// (chain c uses shifts[4 nb c ..]).  Windows are planned on the host (bulge positions
+// are a function of the step); every chain walks the same window sequence, chain c
+// D windows behind chain c-1, D the smallest lag that keeps concurrent windows
+// disjoint.
+//   K = 1: chase(k+1) on `st` overlaps the far part of apply(k) on `aux`; the near
+//          part (columns the next window loads) runs first.
+//   K > 1: per time step one launch chases every active chain (one CTA each), then
+//          one launch applies all their Z to the rows right of the windows and one to
+//          the columns above them and to U (row / column regions of different chains
+//          are disjoint; a row region of one chain meets a column region of the next
+//          only across the two launches).
 template <class S>
-int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const typename tr<S>::R* shifts, S* Zbuf,
-             cudaStream_t st, int* nwin, SweepCtx* sc) {
+int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K, const typename tr<S>::R* shifts,
+             S* Zbuf, cudaStream_t st, int* nwin, SweepCtx* sc) {
   constexpr int W = MsCfg<S>::W;
-  const size_t smem_max = (size_t)(W + 1) * (2 * W + 1) * sizeof(S);  // H window + dummy column, Z
+  const size_t smem_max = (size_t)(W + 1) * (2 * W) * sizeof(S);  // H window + Z, stride W + 1
   MSY_SMEM_ATTR_ONCE(chase_kernel<S>, smem_max);
+  MSY_SMEM_ATTR_ONCE(apply_z_kernel<S>, (int)applyz_smem<S>(W));
+  MSY_SMEM_ATTR_ONCE(apply_z_multi_kernel<S>, (int)applyz_smem<S>(W));
+  if (K < 1 || K > KMAX) return -5;
   const int span = hi - lo;
   const long Tn = 4L * (nb - 1) + span;
   auto Lf = [&](long t) {
@@ -108,7 +119,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
     return (int)std::min<long>(P + 4, hi);
   };
   struct Win { int ws, we, t0, t1; };
-  Win wins[4096];
+  static thread_local Win wins[4096];
   int nwins = 0;
   for (long t = 0; t < Tn;) {
     int ws = Lf(t);
@@ -120,11 +131,98 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, const 
     t = t1;
   }
   const int nthr = 32 * std::max(nb, 4);
+  if (K > 1) {
+    int D = 1;
+    for (bool ok = false; !ok; D++) {
+      ok = true;
+      for (int k = 0; k + D < nwins && ok; k++) ok = wins[k].we <= wins[k + D].ws;
+      if (ok) break;
+    }
+    // per time step tau, on st: chase (all chains) -> near rows -> near columns; on aux:
+    // far rows -> far columns + U, overlapping the next chase.  near(tau) waits for
+    // far(tau-1) (their regions can meet); Z buffers alternate with tau.
+    static const bool mc_serial = getenv("MSY_MC_SERIAL") != nullptr;
+    const bool ovl = sc->aux != nullptr && !mc_serial;
+    cudaStream_t fst = ovl ? sc->aux : st;
+    for (int tau = 0; tau < nwins + (K - 1) * D; tau++) {
+      ChaseJobs<S> cj;
+      ApplyJobs<S> jr[2] = {}, jc[2] = {};  // [0] near, [1] far
+      int nj = 0;
+      // Consistency: a block hit by one chain's row update and another's column update must
+      // see the whole row update first, so near rows reach past every window of this step;
+      // far parts stay clear of the next step's windows (rows >= rstar, columns < cstar).
+      int we_max = 0, rstar = m, cstar = 0;
+      for (int c = 0; c < K; c++) {
+        const int k = tau - c * D, k1 = k + 1;
+        if (k >= 0 && k < nwins) we_max = std::max(we_max, wins[k].we);
+        if (k1 >= 0 && k1 < nwins) { rstar = std::min(rstar, wins[k1].ws); cstar = std::max(cstar, wins[k1].we); }
+      }
+      for (int c = 0; c < K; c++) {
+        const int k = tau - c * D;
+        if (k < 0 || k >= nwins) continue;
+        const Win& w = wins[k];
+        const int nz = w.we - w.ws;
+        S* Zc = Zbuf + ((size_t)2 * c + (tau & 1)) * ZMAX * ZMAX;
+        cj.ws[nj] = w.ws; cj.we[nj] = w.we; cj.t0[nj] = w.t0; cj.t1[nj] = w.t1;
+        cj.shifts[nj] = shifts + 4 * nb * c;
+        cj.Z[nj] = Zc;
+        const int cn = std::min(m, std::max({w.we + W, we_max, cstar}));
+        const int rn = std::max(0, std::min(w.ws - W, rstar));
+        for (int f = 0; f < 2; f++) {
+          ApplyJobs<S>& r = jr[f];
+          r.nz[nj] = nz; r.Z[nj] = Zc; r.r0[nj] = w.ws; r.rR1[nj] = 0; r.mU[nj] = 0;
+          r.cL0[nj] = f == 0 ? w.we : cn;
+          r.cL1[nj] = f == 0 ? cn : m;
+        }
+        // column regions: rows [rn, ws) (near) and [0, rn) + U (far)
+        jc[0].nz[nj] = nz; jc[0].Z[nj] = Zc; jc[0].r0[nj] = w.ws; jc[0].cL0[nj] = jc[0].cL1[nj] = 0;
+        jc[0].rR1[nj] = w.ws; jc[0].mU[nj] = 0;
+        jc[1].nz[nj] = nz; jc[1].Z[nj] = Zc; jc[1].r0[nj] = w.ws; jc[1].cL0[nj] = jc[1].cL1[nj] = 0;
+        jc[1].rR1[nj] = rn; jc[1].mU[nj] = m;
+        jc[0].rlo[nj] = rn;
+        nj++;
+      }
+      if (nj == 0) continue;
+      for (int f = 0; f < 2; f++) {
+        jr[f].n = jc[f].n = nj;
+        jr[f].start[0] = jc[f].start[0] = 0;
+        for (int j = 0; j < nj; j++) {
+          jr[f].start[j + 1] = jr[f].start[j] + (jr[f].cL1[j] > jr[f].cL0[j] ? cdiv(jr[f].cL1[j] - jr[f].cL0[j], 32) : 0);
+          jc[f].start[j + 1] = jc[f].start[j] + (jc[f].rR1[j] > jc[f].rlo[j] ? cdiv(jc[f].rR1[j] - jc[f].rlo[j], 32) : 0) +
+                               cdiv(jc[f].mU[j], 32);
+        }
+      }
+      chase_kernel<S><<<nj, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
+      MSY_LAUNCH_CK();
+      if (ovl && tau > 0) MSY_CK(cudaStreamWaitEvent(st, sc->evD, 0));  // far(tau-1) done
+      for (int f = 0; f < 2; f++) {
+        cudaStream_t s2 = f == 0 ? st : fst;
+        if (f == 1 && ovl) {
+          MSY_CK(cudaEventRecord(sc->evN, st));
+          MSY_CK(cudaStreamWaitEvent(fst, sc->evN, 0));
+        }
+        if (jr[f].start[nj] > 0) {
+          apply_z_multi_kernel<S><<<jr[f].start[nj], 256, applyz_smem<S>(W), s2>>>(H, ldh, U, ldu, jr[f]);
+          MSY_LAUNCH_CK();
+        }
+        if (jc[f].start[nj] > 0) {
+          apply_z_multi_kernel<S><<<jc[f].start[nj], 256, applyz_smem<S>(W), s2>>>(H, ldh, U, ldu, jc[f]);
+          MSY_LAUNCH_CK();
+        }
+      }
+      if (ovl) MSY_CK(cudaEventRecord(sc->evD, fst));
+      if (nwin) (*nwin) += nj;
+    }
+    if (ovl) MSY_CK(cudaStreamWaitEvent(st, sc->evD, 0));
+    return 0;
+  }
   auto chase = [&](int k) -> int {
     const Win& w = wins[k];
-    int nw = w.we - w.ws;
-    chase_kernel<S><<<1, nthr, (size_t)(nw + 1) * (2 * nw + 1) * sizeof(S), st>>>(H, ldh, lo, hi, nb, shifts, w.ws, w.we,
-                                                                            w.t0, w.t1, Zbuf + (k & 1) * ZMAX * ZMAX);
+    ChaseJobs<S> cj;
+    cj.ws[0] = w.ws; cj.we[0] = w.we; cj.t0[0] = w.t0; cj.t1[0] = w.t1;
+    cj.shifts[0] = shifts;
+    cj.Z[0] = Zbuf + (k & 1) * ZMAX * ZMAX;
+    chase_kernel<S><<<1, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
     MSY_LAUNCH_CK();
     if (sc->aux) MSY_CK(cudaEventRecord(sc->evC, st));
     return 0;
@@ -223,7 +321,12 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     }
     if (loc.sweeps >= limit) { loc.status = ST_ITERLIMIT; break; }
     int nb = std::min(MsCfg<S>::NB, std::max(1, (sz - 8) / 8));
-    int ns = 2 * nb;
+    // several chains per sweep when the active block is large and the trailing
+    // block that supplies their shifts fits the one-CTA kernel
+    int K = 1;
+    if (nb == MsCfg<S>::NB && !getenv("MSY_ONE_CHAIN"))
+      K = std::max(1, std::min({KMAX, SmallCfg<S>::NMAX / (2 * nb), sz / (12 * nb)}));
+    int ns = 2 * nb * K;
     bool exc = (stag > 0 && stag % 6 == 0);
     if (!exc) {
       const S* src = A + (hi - ns + 1) + (size_t)(hi - ns + 1) * lda;
@@ -232,10 +335,11 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
       rc = schur_small_launch<S>(ns, w.sblk, ns, nullptr, 0, SS_EIGONLY, w.wr, w.wi, w.dinfo + 16, st);
       if (rc) return rc;
     }
-    pair_shifts_kernel<S><<<1, 32, 0, st>>>(ns, w.wr, w.wi, nb, w.shifts, exc ? 1 : 0, A, lda, lo, hi, w.dinfo + 24);
+    pair_shifts_kernel<S><<<1, 32, 0, st>>>(ns, w.wr, w.wi, nb * K, w.shifts, exc ? 1 : 0, A, lda, lo, hi,
+                                            w.dinfo + 24);
     MSY_LAUNCH_CK();
     pt.lap(&loc.ms_shift);
-    rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, w.shifts, w.Z, st, &loc.windows, sc);
+    rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, K, w.shifts, w.Z, st, &loc.windows, sc);
     if (rc) return rc;
     pt.lap(&loc.ms_sweep);
     loc.sweeps++;

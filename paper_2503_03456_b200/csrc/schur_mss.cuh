@@ -24,12 +24,13 @@ namespace msy {
 template <class S> struct MssCfg { static constexpr int NWARP = 8; };
 constexpr int MSS_A2 = 33;  // ld of the shift-block scratch (<= 32 x 32 plus dummy row/column)
 
-// Eigenvalues of the k x k upper Hessenberg matrix A (smem, column-major, ld,
-// k <= 32; row/column `k` are dummies) by one warp; A is destroyed.
+// Eigenvalues of the k x k upper Hessenberg matrix A (smem, column-major, ld
+// MSS_A2, k <= 32) by one warp; A is destroyed.
 // Returns ST_OK or ST_ITERLIMIT.
 template <class S>
-__device__ int warp_eig(int k, S* A, int ld, typename tr<S>::R* wr, typename tr<S>::R* wi, int lane) {
+__device__ int warp_eig(int k, S* A, typename tr<S>::R* wr, typename tr<S>::R* wi, int lane) {
   typedef typename tr<S>::R R;
+  constexpr int ld = MSS_A2;
   const R u = tr<S>::u();
 #define AA(i, j) A[(i) + (j) * ld]
   int i = k - 1, its = 0, total = 0;
@@ -83,24 +84,13 @@ __device__ int warp_eig(int k, S* A, int ld, typename tr<S>::R* wr, typename tr<
       if (!iszero(tau)) {
         const int rmax = (p + 4 < i) ? p + 4 : i;
         if (nr == 3) {
-          warp_left3<S>(A, ld, p + 1, p + 1, i, k, conj(tau), v1, v2, lane);
+          wl3<S, ld>(A, p + 1, p + 1, i, conj(tau), v1, v2, lane);
           __syncwarp();
-          warp_right3<S>(A, ld, p + 1, l, rmax, k, tau, v1, v2, lane);
+          wr3<S, ld>(A, p + 1, l, rmax, tau, v1, v2, lane);
         } else {
-          const S ctau = conj(tau);
-          for (int c = p + 1 + lane; c <= i; c += 32) {
-            S h0 = AA(p + 1, c), h1 = AA(p + 2, c);
-            S w = ctau * fmacc(v1, h1, h0);
-            AA(p + 1, c) = h0 - w;
-            AA(p + 2, c) = h1 - v1 * w;
-          }
+          wl2<S, ld>(A, p + 1, p + 1, i, conj(tau), v1, lane);
           __syncwarp();
-          for (int r = l + lane; r <= rmax; r += 32) {
-            S a0 = AA(r, p + 1), a1 = AA(r, p + 2);
-            S w = tau * fmac(a1, v1, a0);
-            AA(r, p + 1) = a0 - w;
-            AA(r, p + 2) = a1 - w * conj(v1);
-          }
+          wr2<S, ld>(A, p + 1, l, rmax, tau, v1, lane);
         }
       }
       __syncwarp();
@@ -167,11 +157,11 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
   typedef typename tr<S>::R R;
   constexpr int NW = MssCfg<S>::NWARP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int ld = n + 1;
+  constexpr int ld = SmallCfg<S>::NMAX + 1;  // fixed stride: immediate smem offsets in the warp ops
   const bool wantz = flags & SS_WANTZ;
   const bool eigonly = flags & SS_EIGONLY;
-  S* H = (S*)smem_raw;                        // n rows (+ dummy row n) x (n + 1) columns (dummy column n)
-  S* Zs = H + (size_t)ld * (n + 1);           // ld x n when wantz
+  S* H = (S*)smem_raw;                        // n x n, stride ld
+  S* Zs = H + (size_t)ld * n;                 // n x n when wantz
   S* A2 = Zs + (wantz ? (size_t)ld * n : 0);  // shift block scratch, MSS_A2 x MSS_A2
   __shared__ MssShared<S> sh;
   __shared__ S vbuf[SmallCfg<S>::NMAX + 4];
@@ -291,7 +281,7 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
           A2[r + c * MSS_A2] = (r <= c + 1) ? HH(k0 + r, k0 + c) : S(0);
         }
         __syncwarp();
-        int st = warp_eig<S>(ns, A2, MSS_A2, ewr, ewi, lane);
+        int st = warp_eig<S>(ns, A2, ewr, ewi, lane);
         __syncwarp();
         if (lane == 0) {
           if (st != ST_OK) {  // fall back to the trailing diagonal entry
@@ -323,17 +313,8 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
         refl3_fast(nr, x0, x1, x2, beta, tau, v1, v2);
         __syncwarp();
         if (!iszero(tau)) {
-          if (nr == 3) {
-            warp_left3<S>(H, ld, p + 1, p + 1, jmax, n, conj(tau), v1, v2, lane);
-          } else {
-            const S ctau = conj(tau);
-            for (int c = p + 1 + lane; c <= jmax; c += 32) {
-              S h0 = HH(p + 1, c), h1 = HH(p + 2, c);
-              S w = ctau * fmacc(v1, h1, h0);
-              HH(p + 1, c) = h0 - w;
-              HH(p + 2, c) = h1 - v1 * w;
-            }
-          }
+          if (nr == 3) wl3<S, ld>(H, p + 1, p + 1, jmax, conj(tau), v1, v2, lane);
+          else wl2<S, ld>(H, p + 1, p + 1, jmax, conj(tau), v1, lane);
         }
         if (p >= l && lane == 0) {
           HH(p + 1, p) = beta;
@@ -345,19 +326,11 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
       if (act && !iszero(tau)) {
         const int rmax = (p + 4 < i) ? p + 4 : i;
         if (nr == 3) {
-          warp_right3<S>(H, ld, p + 1, rmin, rmax, n, tau, v1, v2, lane);
-          if (wantz) warp_right3<S>(Zs, ld, p + 1, 0, n - 1, n, tau, v1, v2, lane);
+          wr3<S, ld>(H, p + 1, rmin, rmax, tau, v1, v2, lane);
+          if (wantz) wr3<S, ld>(Zs, p + 1, 0, n - 1, tau, v1, v2, lane);
         } else {
-          for (int pass = 0; pass < (wantz ? 2 : 1); pass++) {
-            S* M = pass == 0 ? H : Zs;
-            const int r0 = pass == 0 ? rmin : 0, r1 = pass == 0 ? rmax : n - 1;
-            for (int r = r0 + lane; r <= r1; r += 32) {
-              S a0 = M[r + (p + 1) * ld], a1 = M[r + (p + 2) * ld];
-              S w = tau * fmac(a1, v1, a0);
-              M[r + (p + 1) * ld] = a0 - w;
-              M[r + (p + 2) * ld] = a1 - w * conj(v1);
-            }
-          }
+          wr2<S, ld>(H, p + 1, rmin, rmax, tau, v1, lane);
+          if (wantz) wr2<S, ld>(Zs, p + 1, 0, n - 1, tau, v1, lane);
         }
       }
       __syncthreads();
@@ -380,7 +353,8 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
 
 template <class S>
 static size_t mss_smem_bytes(int n, bool wantz) {
-  return ((size_t)(n + 1) * (n + 1) + (wantz ? (size_t)(n + 1) * n : 0) + (size_t)MSS_A2 * MSS_A2) * sizeof(S) + 64;
+  const size_t ld = SmallCfg<S>::NMAX + 1;
+  return (ld * n * (wantz ? 2 : 1) + (size_t)MSS_A2 * MSS_A2) * sizeof(S) + 64;
 }
 
 }  // namespace msy
