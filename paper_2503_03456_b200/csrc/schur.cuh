@@ -31,7 +31,7 @@ struct SchurWs {
   static void carve(Arena& ar, int m, SchurWs& w) {
     if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
     w.Z = ar.get<S>((size_t)2 * KMAX * ZMAX * ZMAX);
-    w.sblk = ar.get<S>(128 * 128);
+    w.sblk = ar.get<S>(192 * 192);
     w.wr = ar.get<R>(256);
     w.wi = ar.get<R>(256);
     w.shifts = ar.get<R>(4 * 128);
@@ -324,15 +324,20 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     // several chains per sweep when the active block is large and the trailing
     // block that supplies their shifts fits the one-CTA kernel
     int K = 1;
-    if (nb == MsCfg<S>::NB && !getenv("MSY_ONE_CHAIN"))
-      K = std::max(1, std::min({KMAX, SmallCfg<S>::NMAX / (2 * nb), sz / (12 * nb)}));
+    static const int kmax_env = getenv("MSY_CHAINS") ? atoi(getenv("MSY_CHAINS")) : KMAX;
+    if (nb == MsCfg<S>::NB && kmax_env > 1)
+      K = std::max(1, std::min({std::min(kmax_env, KMAX), EigCfg<S>::NMAX / (2 * nb), sz / (12 * nb)}));
     int ns = 2 * nb * K;
     bool exc = (stag > 0 && stag % 6 == 0);
     if (!exc) {
       const S* src = A + (hi - ns + 1) + (size_t)(hi - ns + 1) * lda;
       copy_block_kernel<S><<<dim3(cdiv(ns, 128), ns), 128, 0, st>>>(ns, src, lda, w.sblk, ns);
       MSY_LAUNCH_CK();
-      rc = schur_small_launch<S>(ns, w.sblk, ns, nullptr, 0, SS_EIGONLY, w.wr, w.wi, w.dinfo + 16, st);
+      // shifts need not be converged to working accuracy: a looser deflation tolerance
+      // cuts the eigenvalue iteration roughly in half
+      static const double stol = getenv("MSY_SHIFT_TOL") ? atof(getenv("MSY_SHIFT_TOL")) : 1e-3;
+      rc = schur_small_launch<S>(ns, w.sblk, ns, nullptr, 0, SS_EIGONLY, w.wr, w.wi, w.dinfo + 16, st,
+                                 (R)std::max<double>(stol, tr<S>::u()));
       if (rc) return rc;
     }
     pair_shifts_kernel<S><<<1, 32, 0, st>>>(ns, w.wr, w.wi, nb * K, w.shifts, exc ? 1 : 0, A, lda, lo, hi,

@@ -22,6 +22,8 @@
 namespace msy {
 
 template <class S> struct MssCfg { static constexpr int NWARP = 8; };
+// largest order of an eigenvalues-only call (no Z: the smem holds one matrix)
+template <class S> struct EigCfg { static constexpr int NMAX = sizeof(S) == 4 ? 192 : (sizeof(S) == 8 ? 144 : 104); };
 constexpr int MSS_A2 = 33;  // ld of the shift-block scratch (<= 32 x 32 plus dummy row/column)
 
 // Eigenvalues of the k x k upper Hessenberg matrix A (smem, column-major, ld
@@ -151,13 +153,14 @@ struct MssShared {
   S bt[2];
 };
 
-template <class S>
+template <class S, int LDC>
 __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S* Zg, int ldz, int flags,
-                                                       typename tr<S>::R* wr, typename tr<S>::R* wi, int* info) {
+                                                       typename tr<S>::R* wr, typename tr<S>::R* wi, int* info,
+                                                       typename tr<S>::R tol) {
   typedef typename tr<S>::R R;
   constexpr int NW = MssCfg<S>::NWARP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int ld = SmallCfg<S>::NMAX + 1;  // fixed stride: immediate smem offsets in the warp ops
+  constexpr int ld = LDC;  // fixed stride: immediate smem offsets in the warp ops
   const bool wantz = flags & SS_WANTZ;
   const bool eigonly = flags & SS_EIGONLY;
   S* H = (S*)smem_raw;                        // n x n, stride ld
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
   __shared__ R sw[4 * NW];                    // bulge shift quadruples
   __shared__ R ewr[2 * NW + 2], ewi[2 * NW + 2];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const R u = tr<S>::u();
+  const R u = tol > R(0) ? tol : tr<S>::u();  // deflation tolerance (looser for shift-only calls)
 #define HH(i, j) H[(i) + (j) * ld]
 #define ZZ(i, j) Zs[(i) + (j) * ld]
   for (int e = tid; e < n * n; e += nt) {
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
 
 template <class S>
 static size_t mss_smem_bytes(int n, bool wantz) {
-  const size_t ld = SmallCfg<S>::NMAX + 1;
+  const size_t ld = (n <= SmallCfg<S>::NMAX ? SmallCfg<S>::NMAX : EigCfg<S>::NMAX) + 1;
   return (ld * n * (wantz ? 2 : 1) + (size_t)MSS_A2 * MSS_A2) * sizeof(S) + 64;
 }
 
