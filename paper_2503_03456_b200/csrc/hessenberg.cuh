@@ -434,6 +434,218 @@ __global__ void __launch_bounds__(HP_TPB) hess_panel_coop_kernel(int m, S* A, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Panel kernel v2 (cooperative, every warp busy).  Per panel column c = k + i:
+//   A  own rows: right update a -= Y[:, :i] V[c, :i]^H; partials of V^H a      | sync
+//   B  w = T^H u; own rows: left update a -= V w; partial |a[c+2:]|^2           | sync
+//   C  reflector (every CTA redundantly); own rows: v, new column c            | sync
+//   D  y = A[:, c+1:] v as (32-row slab x 256-column chunk) units spread over
+//      all CTAs (partials per chunk); own rows: partials of V^H v              | sync
+//   E  own rows: Y[:, i] = tau (y - Y[:, :i] (V^H v)); T[:, i]
+// Rows are owned in 32-row slabs (slab s by CTA s mod G).  The gemv units keep
+// 16 column loads per thread in flight, so the BLAS-2 half runs near L2 bandwidth.
+constexpr int HP2_CW = 256;
+template <class S>
+__global__ void __launch_bounds__(HP_TPB) hess_panel2_kernel(int m, S* A, int lda, int k, int nbp, S* V, int ldv,
+                                                             S* Y, int ldy, S* T, int ldt, S* tau, S* red1, S* red2,
+                                                             typename tr<S>::R* redR, S* slot, S* ypart) {
+  typedef typename tr<S>::R R;
+  constexpr int NWP = HP_TPB / 32;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S* sv = (S*)smem_raw;  // v (m entries, zero above row c+1)
+  __shared__ S s_a[HP_ROWS], s_u[HESS_NB], s_w[HESS_NB], s_acc[HESS_NB];
+  __shared__ S s_part[NWP][32];
+  __shared__ S s_beta, s_tau, s_scal;
+  __shared__ R s_rsum[NWP];
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nslab = cdiv(m, HP_ROWS);
+  const S* Vp = V + (size_t)k * ldv;
+  for (int i = 0; i < nbp; i++) {
+    const int c = k + i;
+    S* ac = A + (size_t)c * lda;
+    if (i > 0) {
+      // ---- A ----
+      if (tid < HESS_NB) s_acc[tid] = S(0);
+      if (tid < i) s_w[tid] = conj(Vp[c + (size_t)tid * ldv]);  // row c of V (conjugated)
+      __syncthreads();
+      for (int sl = g; sl < nslab; sl += G) {
+        const int r = sl * HP_ROWS + lane;
+        if (warp == 0) {
+          S a = S(0);
+          if (r < m) {
+            a = ac[r];
+            S t[HESS_NB];
+#pragma unroll
+            for (int q = 0; q < HESS_NB; q++) t[q] = q < i ? Y[r + (size_t)q * ldy] : S(0);
+#pragma unroll
+            for (int q = 0; q < HESS_NB; q++) if (q < i) a = a - t[q] * s_w[q];
+            ac[r] = a;
+          }
+          s_a[lane] = (r < m && r >= k + 1) ? a : S(0);
+        }
+        __syncthreads();
+        for (int q = warp; q < i; q += NWP) {
+          S val = (r < m) ? conj(Vp[r + (size_t)q * ldv]) * s_a[lane] : S(0);
+          val = warp_sum(val);
+          if (lane == 0) s_acc[q] += val;
+        }
+        __syncthreads();
+      }
+      if (tid < HESS_NB) red1[g * HESS_NB + tid] = s_acc[tid];
+      grid.sync();
+      // ---- B ----
+      cta_sum_partials<S>(red1, G, i, s_u, s_part);
+      if (tid < i) {  // w = T^H u
+        S sum = S(0);
+        for (int q = 0; q <= tid; q++) sum = fmacc(T[q + tid * ldt], s_u[q], sum);
+        s_w[tid] = sum;
+      }
+      __syncthreads();
+    }
+    {
+      R nrm = 0;
+      if (warp == 0) {
+        for (int sl = g; sl < nslab; sl += G) {
+          const int r = sl * HP_ROWS + lane;
+          if (r < m) {
+            S a = ac[r];
+            if (i > 0 && r >= k + 1) {
+              S t[HESS_NB];
+#pragma unroll
+              for (int q = 0; q < HESS_NB; q++) t[q] = q < i ? Vp[r + (size_t)q * ldv] : S(0);
+#pragma unroll
+              for (int q = 0; q < HESS_NB; q++) if (q < i) a = a - t[q] * s_w[q];
+              ac[r] = a;
+            }
+            if (r >= c + 2) nrm += abs2(a);
+            if (r == c + 1) *slot = a;
+          }
+        }
+        nrm = warp_sum(nrm);
+        if (lane == 0) redR[g] = nrm;
+      }
+    }
+    grid.sync();
+    // ---- C ----
+    {
+      R t = 0;
+      for (int gg = tid; gg < G; gg += HP_TPB) t += redR[gg];
+      t = warp_sum(t);
+      if (lane == 0) s_rsum[warp] = t;
+      __syncthreads();
+      if (tid == 0) {
+        R tt = 0;
+#pragma unroll
+        for (int w8 = 0; w8 < NWP; w8++) tt += s_rsum[w8];
+        S x0 = *slot;
+        if (tt == R(0) && im(x0) == R(0)) {
+          s_tau = S(0); s_beta = x0; s_scal = S(0);
+        } else {
+          R nrmv = sqrt(abs2(x0) + tt);
+          R b = re(x0) >= R(0) ? -nrmv : nrmv;
+          s_beta = mk<S>(b);
+          s_tau = (mk<S>(b) - x0) / mk<S>(b);
+          s_scal = S(1) / (x0 - mk<S>(b));
+        }
+      }
+      __syncthreads();
+      S* vc = V + (size_t)c * ldv;
+      const S scal = s_scal, beta = s_beta;
+      if (warp == 0)
+        for (int sl = g; sl < nslab; sl += G) {
+          const int r = sl * HP_ROWS + lane;
+          if (r < m && r >= c + 1) {
+            S a = ac[r];
+            vc[r] = (r == c + 1) ? S(1) : a * scal;
+            ac[r] = (r == c + 1) ? beta : S(0);
+          }
+        }
+      if (g == 0 && tid == 0) { tau[c] = s_tau; T[i + i * ldt] = s_tau; }
+    }
+    grid.sync();
+    // ---- D ----
+    {
+      const S* vc = V + (size_t)c * ldv;
+      for (int q = tid; q < m; q += HP_TPB) sv[q] = q >= c + 1 ? vc[q] : S(0);
+      __syncthreads();
+      const int q0 = c + 1, nq = m - q0;
+      const int nch = cdiv(nq, HP2_CW);
+      const int units = nslab * nch;
+      for (int u = g; u < units; u += G) {
+        const int sl = u % nslab, cc = u / nslab;
+        const int r = sl * HP_ROWS + lane, rr = r < m ? r : m - 1;
+        const int qa = q0 + cc * HP2_CW, qb = min(qa + HP2_CW, m);
+        constexpr int UB = HP2_CW / NWP;  // columns per warp (16)
+        S a[UB];
+#pragma unroll
+        for (int j = 0; j < UB; j++) {
+          const int q = qa + warp + NWP * j;
+          a[j] = q < qb ? A[rr + (size_t)q * lda] : S(0);
+        }
+        S acc0 = S(0), acc1 = S(0);
+#pragma unroll
+        for (int j = 0; j < UB; j += 2) {
+          const int q = qa + warp + NWP * j;
+          acc0 = fmac(a[j], q < qb ? sv[q] : S(0), acc0);
+          acc1 = fmac(a[j + 1], q + NWP < qb ? sv[q + NWP] : S(0), acc1);
+        }
+        s_part[warp][lane] = acc0 + acc1;
+        __syncthreads();
+        if (warp == 0 && r < m) {
+          S y = S(0);
+#pragma unroll
+          for (int w = 0; w < NWP; w++) y += s_part[w][lane];
+          ypart[(size_t)cc * m + r] = y;
+        }
+        __syncthreads();
+      }
+      if (i > 0) {  // partials of V[:, :i]^H v over own rows (v = 0 above row c+1)
+        if (tid < HESS_NB) s_acc[tid] = S(0);
+        __syncthreads();
+        for (int sl = g; sl < nslab; sl += G) {
+          const int r = sl * HP_ROWS + lane;
+          for (int q = warp; q < i; q += NWP) {
+            S val = (r < m && r >= c + 1) ? conj(Vp[r + (size_t)q * ldv]) * sv[r] : S(0);
+            val = warp_sum(val);
+            if (lane == 0) s_acc[q] += val;
+          }
+        }
+        __syncthreads();
+        if (tid < HESS_NB) red2[g * HESS_NB + tid] = s_acc[tid];
+      }
+    }
+    grid.sync();
+    // ---- E ----
+    {
+      if (i > 0) cta_sum_partials<S>(red2, G, i, s_u, s_part);
+      const int nch = cdiv(m - (c + 1), HP2_CW);
+      const S ti = s_tau;
+      if (warp == 0)
+        for (int sl = g; sl < nslab; sl += G) {
+          const int r = sl * HP_ROWS + lane;
+          if (r < m) {
+            S y = S(0);
+            for (int cc = 0; cc < nch; cc++) y += ypart[(size_t)cc * m + r];
+            S t[HESS_NB];
+#pragma unroll
+            for (int q = 0; q < HESS_NB; q++) t[q] = q < i ? Y[r + (size_t)q * ldy] : S(0);
+#pragma unroll
+            for (int q = 0; q < HESS_NB; q++) y = y - t[q] * (q < i ? s_u[q] : S(0));
+            Y[r + (size_t)i * ldy] = ti * y;
+          }
+        }
+      if (g == 0 && tid < i) {
+        S sum = S(0);
+        for (int q = tid; q < i; q++) sum = fmac(T[tid + q * ldt], s_u[q], sum);
+        T[tid + i * ldt] = -(ti * sum);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <class S>
 struct HessWs {
   S *V, *Y, *T, *part, *tau, *W1, *W2, *red1, *red2, *slot, *skp;
@@ -453,6 +665,21 @@ struct HessWs {
     w.skp = ar.get<S>((size_t)HESS_SPLITK * HESS_NB * m);
   }
 };
+
+// grid size of the v2 panel kernel: enough CTAs for the gemv units, all co-resident
+template <class S>
+int hess2_grid(int m) {
+  int dev, nsm, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = (size_t)m * sizeof(S);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(hess_panel2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hess_panel2_kernel<S>, HP_TPB, smem) != cudaSuccess)
+    return 0;
+  const int nslab = cdiv(m, HP_ROWS), units = nslab * cdiv(m, HP2_CW);
+  return std::min(per * nsm, std::max(nslab, std::min(units, nsm)));
+}
 
 // grid size of the cooperative panel kernel (0 if it cannot be co-resident)
 template <class S>
@@ -477,7 +704,8 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
   zero_kernel<S><<<cdiv((size_t)m * m, 256), 256, 0, st>>>((size_t)m * m, w.V);
   MSY_LAUNCH_CK();
   const int last = m - 3;  // last column that gets a reflector
-  const int G = getenv("MSY_HESS_NOCOOP") ? 0 : hess_coop_grid<S>(m);
+  static const int hmode = getenv("MSY_HESS_MODE") ? atoi(getenv("MSY_HESS_MODE")) : 2;  // 0 none, 1 v1, 2 v2
+  const int G = hmode == 0 ? 0 : (hmode == 1 ? hess_coop_grid<S>(m) : hess2_grid<S>(m));
   int np = 0;
   for (int k = 0; k <= last; k += HESS_NB, np++) {
     const int nbp = min(HESS_NB, last - k + 1);
@@ -488,9 +716,10 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
       int mm = m, ldaa = lda, kk = k, nb_ = nbp, ldvv = ldv, ldyy = ldy, ldtt = ldt;
       S *Vv = w.V, *Yy = w.Y, *Tt = T, *ta = w.tau, *r1 = w.red1, *r2 = w.red2, *sl = w.slot;
       typename tr<S>::R* rR = w.redR;
-      void* args[] = {&mm, &Ap, &ldaa, &kk, &nb_, &Vv, &ldvv, &Yy, &ldyy, &Tt, &ldtt, &ta, &r1, &r2, &rR, &sl};
-      MSY_CK(cudaLaunchCooperativeKernel((const void*)hess_panel_coop_kernel<S>, dim3(G), dim3(HP_TPB), args,
-                                         (size_t)m * sizeof(S), st));
+      S* yp = w.part;
+      void* args[] = {&mm, &Ap, &ldaa, &kk, &nb_, &Vv, &ldvv, &Yy, &ldyy, &Tt, &ldtt, &ta, &r1, &r2, &rR, &sl, &yp};
+      const void* fn = hmode == 1 ? (const void*)hess_panel_coop_kernel<S> : (const void*)hess_panel2_kernel<S>;
+      MSY_CK(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(HP_TPB), args, (size_t)m * sizeof(S), st));
       MSY_LAUNCH_CK();
     }
     for (int i = 0; i < nbp && G == 0; i++) {

@@ -137,18 +137,41 @@ __device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int 
   return ok;
 }
 
+constexpr int TRS_TPB = 256;  // 2 CTAs per SM: the update of one block overlaps another's loads
 template <class S>
-__global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
+__global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
                                                          const S* __restrict__ TB, int ldb, int lowerB, S* W, int ldw,
                                                          const int* __restrict__ rb, const int* __restrict__ cb, int nbi,
                                                          int nbj, int d, int* status) {
   constexpr int NB = TrsylCfg<S>::NB;
-  constexpr int MT = (NB + 1 + 3) / 4;  // micro-tile grid (MT x MT threads, 4x4 each)
-  constexpr int P = 4 * MT;             // padded tile edge
-  const int I = blockIdx.y, J = blockIdx.x;
-  const int rI = nbi - 1 - I, cJ = lowerB ? nbj - 1 - J : J;
+  constexpr int P = 4 * ((NB + 1 + 3) / 4);  // padded tile edge (smem stride)
+  constexpr int TG = 16;                     // 16 x 16 threads, RM x RM accumulators each
+  constexpr int RM = (NB + 1 + TG - 1) / TG;
+  // blockIdx.x enumerates the blocks that change at step d (rank space: rI = row rank from
+  // the bottom, cJ = column rank in solve order): rows rI < d with cJ >= d - rI, then
+  // columns cJ < d with rI >= d; at d = 0 the single block (0, 0).  Blocks with rI >= d
+  // and cJ >= d receive nothing yet and are not launched.
+  int rI, cJ;
+  {
+    int b = blockIdx.x;
+    if (d == 0) { rI = 0; cJ = 0; }
+    else {
+      const int ra = min(d, nbi);
+      rI = -1;
+      for (int r = 0; r < ra; r++) {
+        const int len = max(0, nbj - max(0, d - r));
+        if (b < len) { rI = r; cJ = max(0, d - r) + b; break; }
+        b -= len;
+      }
+      if (rI < 0) {  // second part: columns cJ < d, rows rI >= d
+        const int h = nbi - d;
+        cJ = b / h;
+        rI = d + b % h;
+      }
+    }
+  }
+  const int I = nbi - 1 - rI, J = lowerB ? nbj - 1 - cJ : cJ;
   const int dd = rI + cJ;
-  if (dd < d) return;
   const int i0 = rb[I], i1 = rb[I + 1], j0 = cb[J], j1 = cb[J + 1];
   const int bi = i1 - i0, bj = j1 - j0;
   if (bi <= 0 || bj <= 0) return;
@@ -160,13 +183,29 @@ __global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const 
   __shared__ int ru_of[NB + 2], cu_of[NB + 2];  // rank -> first row / column of the unit
   __shared__ int nru, ncu;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int tr_ = tid % MT, tc = tid / MT;
-  const bool mt_act = tid < MT * MT;
-  S acc[4][4];
+  const int tr_ = tid % TG, tc = tid / TG;
+  S acc[RM][RM];
 #pragma unroll
-  for (int a = 0; a < 4; a++)
+  for (int a = 0; a < RM; a++)
 #pragma unroll
-    for (int b = 0; b < 4; b++) acc[a][b] = S(0);
+    for (int b = 0; b < RM; b++) acc[a][b] = S(0);
+  // rank-bk update acc += As[:, k] Bs[k, :]; entries past the block edge accumulate
+  // garbage in accumulators that are never written back, so the tiles need no zero fill
+  auto mm = [&](int bk) {
+    for (int k = 0; k < bk; k++) {
+      S a[RM], b[RM];
+#pragma unroll
+      for (int q = 0; q < RM; q++) {
+        const int i = min(tr_ + TG * q, P - 1), j = min(tc + TG * q, P - 1);
+        a[q] = As[k * P + i];
+        b[q] = Bs[k * P + j];
+      }
+#pragma unroll
+      for (int x = 0; x < RM; x++)
+#pragma unroll
+        for (int y = 0; y < RM; y++) acc[x][y] = fmac(a[x], b[y], acc[x][y]);
+    }
+  };
 
   // ---- updates from diagonal d-1 ----
   if (d >= 1) {
@@ -175,8 +214,6 @@ __global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const 
     if (ra >= 0 && ra < rI) {
       int Is = nbi - 1 - ra;
       int k0 = rb[Is], k1 = rb[Is + 1], bk = k1 - k0;
-      for (int e = tid; e < P * P; e += nt) { As[e] = S(0); Bs[e] = S(0); }
-      __syncthreads();
       for (int e = tid; e < bi * bk; e += nt) {
         int i = e % bi, k = e / bi;
         As[k * P + i] = TA[(i0 + i) + (size_t)(k0 + k) * lda];
@@ -186,17 +223,7 @@ __global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const 
         Bs[k * P + j] = W[(k0 + k) + (size_t)(j0 + j) * ldw];
       }
       __syncthreads();
-      if (mt_act) {
-        for (int k = 0; k < bk; k++) {
-          S a[4], b[4];
-#pragma unroll
-          for (int q = 0; q < 4; q++) { a[q] = As[k * P + tr_ + MT * q]; b[q] = Bs[k * P + tc + MT * q]; }
-#pragma unroll
-          for (int x = 0; x < 4; x++)
-#pragma unroll
-            for (int y = 0; y < 4; y++) acc[x][y] = fmac(a[x], b[y], acc[x][y]);
-        }
-      }
+      mm(bk);
       __syncthreads();
     }
     // B-part: W -= Y[I, J*] TB[J*, J], with rank(J*) = d-1-rI
@@ -204,8 +231,6 @@ __global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const 
     if (cr >= 0 && cr < cJ) {
       int Js = lowerB ? nbj - 1 - cr : cr;
       int k0 = cb[Js], k1 = cb[Js + 1], bk = k1 - k0;
-      for (int e = tid; e < P * P; e += nt) { As[e] = S(0); Bs[e] = S(0); }
-      __syncthreads();
       for (int e = tid; e < bi * bk; e += nt) {
         int i = e % bi, k = e / bi;
         As[k * P + i] = W[(i0 + i) + (size_t)(k0 + k) * ldw];
@@ -215,30 +240,20 @@ __global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const 
         Bs[k * P + j] = TB[(k0 + k) + (size_t)(j0 + j) * ldb];
       }
       __syncthreads();
-      if (mt_act) {
-        for (int k = 0; k < bk; k++) {
-          S a[4], b[4];
-#pragma unroll
-          for (int q = 0; q < 4; q++) { a[q] = As[k * P + tr_ + MT * q]; b[q] = Bs[k * P + tc + MT * q]; }
-#pragma unroll
-          for (int x = 0; x < 4; x++)
-#pragma unroll
-            for (int y = 0; y < 4; y++) acc[x][y] = fmac(a[x], b[y], acc[x][y]);
-        }
-      }
+      mm(bk);
       __syncthreads();
     }
   }
   // ---- write back the updated W (or stage it for the leaf solve) ----
   const bool solve = (dd == d);
-  if (mt_act) {
+  {
 #pragma unroll
-    for (int x = 0; x < 4; x++) {
-      int i = tr_ + MT * x;
+    for (int x = 0; x < RM; x++) {
+      int i = tr_ + TG * x;
       if (i >= bi) continue;
 #pragma unroll
-      for (int y = 0; y < 4; y++) {
-        int j = tc + MT * y;
+      for (int y = 0; y < RM; y++) {
+        int j = tc + TG * y;
         if (j >= bj) continue;
         S v = W[(i0 + i) + (size_t)(j0 + j) * ldw] - acc[x][y];
         if (solve) Ws[i + j * P] = v;
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(512, 1) trsyl_step_kernel(int m, int n, const 
     ncu = cnt;
   }
   __syncthreads();
-  constexpr int EPT = ((NB + 1) * (NB + 1) + 511) / 512;  // entries per thread (512 threads)
+  constexpr int EPT = ((NB + 1) * (NB + 1) + TRS_TPB - 1) / TRS_TPB;  // entries per thread
   int ei[EPT], ej[EPT], era[EPT], ecr[EPT];
 #pragma unroll
   for (int k = 0; k < EPT; k++) {
@@ -398,8 +413,16 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
                                                                           nbi, w.cb, nbj);
   MSY_LAUNCH_CK();
   for (int d = 0; d < nbi + nbj - 1; d++) {
-    trsyl_step_kernel<S><<<dim3(nbj, nbi), 512, trsyl_smem<S>(), st>>>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb,
-                                                                       w.cb, nbi, nbj, d, status);
+    // blocks changed at step d (see trsyl_step_kernel)
+    long cnt = 0;
+    if (d == 0) cnt = 1;
+    else {
+      for (int r = 0; r < std::min(d, nbi); r++) cnt += std::max(0, nbj - std::max(0, d - r));
+      cnt += (long)std::min(d, nbj) * std::max(0, nbi - d);
+    }
+    if (cnt == 0) continue;
+    trsyl_step_kernel<S><<<(unsigned)cnt, TRS_TPB, trsyl_smem<S>(), st>>>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb, w.cb,
+                                                                      nbi, nbj, d, status);
     MSY_LAUNCH_CK();
   }
   return 0;
