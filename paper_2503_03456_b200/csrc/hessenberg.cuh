@@ -14,6 +14,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -435,16 +437,39 @@ __global__ void __launch_bounds__(HP_TPB) hess_panel_coop_kernel(int m, S* A, in
 }
 
 // ---------------------------------------------------------------------------
-// Panel kernel v2 (cooperative, every warp busy).  Per panel column c = k + i:
-//   A  own rows: right update a -= Y[:, :i] V[c, :i]^H; partials of V^H a      | sync
-//   B  w = T^H u; own rows: left update a -= V w; partial |a[c+2:]|^2           | sync
-//   C  reflector (every CTA redundantly); own rows: v, new column c            | sync
-//   D  y = A[:, c+1:] v as (32-row slab x 256-column chunk) units spread over
-//      all CTAs (partials per chunk); own rows: partials of V^H v              | sync
-//   E  own rows: Y[:, i] = tau (y - Y[:, :i] (V^H v)); T[:, i]
-// Rows are owned in 32-row slabs (slab s by CTA s mod G).  The gemv units keep
-// 16 column loads per thread in flight, so the BLAS-2 half runs near L2 bandwidth.
+// Panel kernel v2 (cooperative).  Rows are owned in 32-row slabs (slab s by CTA
+// s mod G, at most HP2_OWN per CTA); each CTA caches its rows of the panel's V and
+// Y, and a copy of T, in shared memory, so the per-column vector phases touch
+// global memory only for column c itself.  Per panel column c = k + i:
+//   A  own rows: a = A[:, c] - Y[:, :i] V[c, :i]^H; partials of V^H a          | sync
+//   B  w = T^H u; own rows: a -= V w; column c back to HBM; partial norm       | sync
+//   CD every CTA: reflector, v from column c (all rows), own rows of V[:, c];
+//      y = A[:, c+1:] v as (slab x 256-column) units over all CTAs (float4
+//      loads on the fp32 path); own rows: partials of V^H v                    | sync
+//   E  own rows: Y[:, i] = tau (y - Y[:, :i] (V^H v)); column c := (beta, 0..);
+//      T[:, i] (every CTA in smem, CTA 0 to HBM)
 constexpr int HP2_CW = 256;
+constexpr int HP2_OWN = 4;
+constexpr int HP2_LD = HESS_NB + 1;
+#ifdef MSY_HESS_PROF
+__device__ unsigned long long g_hess_prof[8];
+#define HPROF(slot)                                                                          \
+  do {                                                                                       \
+    if (g == 0 && tid == 0) {                                                                \
+      unsigned long long t_;                                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                 \
+      if (slot > 0) atomicAdd(&g_hess_prof[slot], t_ - t_prev_);                             \
+      t_prev_ = t_;                                                                          \
+    }                                                                                        \
+  } while (0)
+#else
+#define HPROF(slot) do {} while (0)
+#endif
+template <class S>
+static size_t hess2_smem(int m) {
+  return ((size_t)m + 2 * (size_t)HP2_OWN * HESS_NB * HP2_LD + (size_t)HESS_NB * HP2_LD + (size_t)HP2_OWN * HP_ROWS) *
+         sizeof(S);
+}
 template <class S>
 __global__ void __launch_bounds__(HP_TPB) hess_panel2_kernel(int m, S* A, int lda, int k, int nbp, S* V, int ldv,
                                                              S* Y, int ldy, S* T, int ldt, S* tau, S* red1, S* red2,
@@ -453,82 +478,92 @@ __global__ void __launch_bounds__(HP_TPB) hess_panel2_kernel(int m, S* A, int ld
   constexpr int NWP = HP_TPB / 32;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  S* sv = (S*)smem_raw;  // v (m entries, zero above row c+1)
-  __shared__ S s_a[HP_ROWS], s_u[HESS_NB], s_w[HESS_NB], s_acc[HESS_NB];
+  S* sv = (S*)smem_raw;                              // v (m entries, zero above row c+1)
+  S* Vc = sv + m;                                    // [own][q][row]: own rows of V[:, k:k+nb]
+  S* Yc = Vc + HP2_OWN * HESS_NB * HP2_LD;           // [own][q][row]: own rows of Y
+  S* Tc = Yc + HP2_OWN * HESS_NB * HP2_LD;           // T, [q][p] = T(q, p)
+  S* scol = Tc + HESS_NB * HP2_LD;                   // [own][row]: own rows of column c
+  __shared__ S s_u[HESS_NB], s_w[HESS_NB], s_acc[HESS_NB];
   __shared__ S s_part[NWP][32];
+  __shared__ float s_p4[NWP][128];  // float4 gemv partials (fp32 path)
   __shared__ S s_beta, s_tau, s_scal;
   __shared__ R s_rsum[NWP];
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nslab = cdiv(m, HP_ROWS);
+  const int nown = g < nslab ? (nslab - 1 - g) / G + 1 : 0;
   const S* Vp = V + (size_t)k * ldv;
+#define VC(o, q) Vc[((o) * HESS_NB + (q)) * HP2_LD + lane]
+#define YC(o, q) Yc[((o) * HESS_NB + (q)) * HP2_LD + lane]
+#ifdef MSY_HESS_PROF
+  unsigned long long t_prev_ = 0;
+#endif
+  HPROF(0);
+  for (int e = tid; e < HESS_NB * HP2_LD; e += HP_TPB) Tc[e] = S(0);
+  __syncthreads();
   for (int i = 0; i < nbp; i++) {
     const int c = k + i;
     S* ac = A + (size_t)c * lda;
+    // ---- A ----
+    if (warp == 0)
+      for (int o = 0; o < nown; o++) {
+        const int r = (g + o * G) * HP_ROWS + lane;
+        scol[o * HP_ROWS + lane] = r < m ? ac[r] : S(0);
+      }
     if (i > 0) {
-      // ---- A ----
       if (tid < HESS_NB) s_acc[tid] = S(0);
       if (tid < i) s_w[tid] = conj(Vp[c + (size_t)tid * ldv]);  // row c of V (conjugated)
       __syncthreads();
-      for (int sl = g; sl < nslab; sl += G) {
-        const int r = sl * HP_ROWS + lane;
-        if (warp == 0) {
-          S a = S(0);
-          if (r < m) {
-            a = ac[r];
-            S t[HESS_NB];
-#pragma unroll
-            for (int q = 0; q < HESS_NB; q++) t[q] = q < i ? Y[r + (size_t)q * ldy] : S(0);
-#pragma unroll
-            for (int q = 0; q < HESS_NB; q++) if (q < i) a = a - t[q] * s_w[q];
-            ac[r] = a;
-          }
-          s_a[lane] = (r < m && r >= k + 1) ? a : S(0);
+      if (warp == 0)
+        for (int o = 0; o < nown; o++) {
+          S a = scol[o * HP_ROWS + lane];
+          for (int q = 0; q < i; q++) a = a - YC(o, q) * s_w[q];
+          scol[o * HP_ROWS + lane] = a;
         }
-        __syncthreads();
+      __syncthreads();
+      for (int o = 0; o < nown; o++) {
+        const int r = (g + o * G) * HP_ROWS + lane;
+        const S a = (r < m && r >= k + 1) ? scol[o * HP_ROWS + lane] : S(0);
         for (int q = warp; q < i; q += NWP) {
-          S val = (r < m) ? conj(Vp[r + (size_t)q * ldv]) * s_a[lane] : S(0);
-          val = warp_sum(val);
+          S val = warp_sum(conj(VC(o, q)) * a);
           if (lane == 0) s_acc[q] += val;
         }
-        __syncthreads();
       }
+      __syncthreads();
       if (tid < HESS_NB) red1[g * HESS_NB + tid] = s_acc[tid];
+      HPROF(1);
       grid.sync();
+      HPROF(2);
       // ---- B ----
       cta_sum_partials<S>(red1, G, i, s_u, s_part);
       if (tid < i) {  // w = T^H u
         S sum = S(0);
-        for (int q = 0; q <= tid; q++) sum = fmacc(T[q + tid * ldt], s_u[q], sum);
+        for (int q = 0; q <= tid; q++) sum = fmacc(Tc[q * HP2_LD + tid], s_u[q], sum);
         s_w[tid] = sum;
       }
-      __syncthreads();
     }
-    {
+    __syncthreads();
+    if (warp == 0) {
       R nrm = 0;
-      if (warp == 0) {
-        for (int sl = g; sl < nslab; sl += G) {
-          const int r = sl * HP_ROWS + lane;
-          if (r < m) {
-            S a = ac[r];
-            if (i > 0 && r >= k + 1) {
-              S t[HESS_NB];
-#pragma unroll
-              for (int q = 0; q < HESS_NB; q++) t[q] = q < i ? Vp[r + (size_t)q * ldv] : S(0);
-#pragma unroll
-              for (int q = 0; q < HESS_NB; q++) if (q < i) a = a - t[q] * s_w[q];
-              ac[r] = a;
-            }
-            if (r >= c + 2) nrm += abs2(a);
-            if (r == c + 1) *slot = a;
-          }
+      for (int o = 0; o < nown; o++) {
+        const int r = (g + o * G) * HP_ROWS + lane;
+        S a = scol[o * HP_ROWS + lane];
+        if (i > 0 && r >= k + 1)
+          for (int q = 0; q < i; q++) a = a - VC(o, q) * s_w[q];
+        if (r < m) {
+          scol[o * HP_ROWS + lane] = a;
+          ac[r] = a;
+          if (r >= c + 2) nrm += abs2(a);
+          if (r == c + 1) *slot = a;
         }
-        nrm = warp_sum(nrm);
-        if (lane == 0) redR[g] = nrm;
       }
+      nrm = warp_sum(nrm);
+      if (lane == 0) redR[g] = nrm;
     }
+    HPROF(3);
     grid.sync();
-    // ---- C ----
+    HPROF(4);
+    // ---- CD ----
     {
       R t = 0;
       for (int gg = tid; gg < G; gg += HP_TPB) t += redR[gg];
@@ -549,66 +584,110 @@ __global__ void __launch_bounds__(HP_TPB) hess_panel2_kernel(int m, S* A, int ld
           s_tau = (mk<S>(b) - x0) / mk<S>(b);
           s_scal = S(1) / (x0 - mk<S>(b));
         }
+        Tc[i * HP2_LD + i] = s_tau;
       }
       __syncthreads();
-      S* vc = V + (size_t)c * ldv;
-      const S scal = s_scal, beta = s_beta;
-      if (warp == 0)
-        for (int sl = g; sl < nslab; sl += G) {
-          const int r = sl * HP_ROWS + lane;
-          if (r < m && r >= c + 1) {
-            S a = ac[r];
-            vc[r] = (r == c + 1) ? S(1) : a * scal;
-            ac[r] = (r == c + 1) ? beta : S(0);
-          }
-        }
+      const S scal = s_scal;
+      for (int q = tid; q < m; q += HP_TPB) sv[q] = q > c + 1 ? ac[q] * scal : (q == c + 1 ? S(1) : S(0));
       if (g == 0 && tid == 0) { tau[c] = s_tau; T[i + i * ldt] = s_tau; }
-    }
-    grid.sync();
-    // ---- D ----
-    {
-      const S* vc = V + (size_t)c * ldv;
-      for (int q = tid; q < m; q += HP_TPB) sv[q] = q >= c + 1 ? vc[q] : S(0);
       __syncthreads();
+      if (warp == 0)
+        for (int o = 0; o < nown; o++) {
+          const int r = (g + o * G) * HP_ROWS + lane;
+          const S vr = r < m ? sv[r] : S(0);
+          VC(o, i) = vr;
+          if (r < m && r >= c + 1) V[r + (size_t)c * ldv] = vr;
+        }
       const int q0 = c + 1, nq = m - q0;
       const int nch = cdiv(nq, HP2_CW);
-      const int units = nslab * nch;
-      for (int u = g; u < units; u += G) {
-        const int sl = u % nslab, cc = u / nslab;
-        const int r = sl * HP_ROWS + lane, rr = r < m ? r : m - 1;
-        const int qa = q0 + cc * HP2_CW, qb = min(qa + HP2_CW, m);
-        constexpr int UB = HP2_CW / NWP;  // columns per warp (16)
-        S a[UB];
+      bool vec = false;
+      if constexpr (std::is_same<S, float>::value)
+        vec = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+      if (vec) {
+        if constexpr (std::is_same<S, float>::value) {
+          // 128-row units: lane loads rows 4 lane .. 4 lane + 3 of each column as one float4
+          const int nsl4 = cdiv(m, 128), units = nsl4 * nch;
+          for (int u = g; u < units; u += G) {
+            const int sl = u % nsl4, cc = u / nsl4;
+            const int r4 = sl * 128 + 4 * lane;
+            const int qa = q0 + cc * HP2_CW, qb = min(qa + HP2_CW, m);
+            constexpr int UB = HP2_CW / NWP;
+            float4 av[UB];
 #pragma unroll
-        for (int j = 0; j < UB; j++) {
-          const int q = qa + warp + NWP * j;
-          a[j] = q < qb ? A[rr + (size_t)q * lda] : S(0);
-        }
-        S acc0 = S(0), acc1 = S(0);
+            for (int j = 0; j < UB; j++) {
+              const int q = qa + warp + NWP * j;
+              if (q < qb && r4 + 3 < m) {
+                av[j] = *reinterpret_cast<const float4*>(A + r4 + (size_t)q * lda);
+              } else if (q < qb) {
+                const float* col = A + (size_t)q * lda;
+                av[j] = make_float4(r4 < m ? col[r4] : 0.f, r4 + 1 < m ? col[r4 + 1] : 0.f,
+                                    r4 + 2 < m ? col[r4 + 2] : 0.f, 0.f);
+              } else {
+                av[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+            }
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < UB; j += 2) {
-          const int q = qa + warp + NWP * j;
-          acc0 = fmac(a[j], q < qb ? sv[q] : S(0), acc0);
-          acc1 = fmac(a[j + 1], q + NWP < qb ? sv[q + NWP] : S(0), acc1);
-        }
-        s_part[warp][lane] = acc0 + acc1;
-        __syncthreads();
-        if (warp == 0 && r < m) {
-          S y = S(0);
+            for (int j = 0; j < UB; j++) {
+              const int q = qa + warp + NWP * j;
+              const float vq = q < qb ? sv[q] : 0.f;
+              acc.x = fmaf(av[j].x, vq, acc.x); acc.y = fmaf(av[j].y, vq, acc.y);
+              acc.z = fmaf(av[j].z, vq, acc.z); acc.w = fmaf(av[j].w, vq, acc.w);
+            }
+            s_p4[warp][4 * lane] = acc.x; s_p4[warp][4 * lane + 1] = acc.y;
+            s_p4[warp][4 * lane + 2] = acc.z; s_p4[warp][4 * lane + 3] = acc.w;
+            __syncthreads();
+            if (tid < 128) {
+              const int row = sl * 128 + tid;
+              if (row < m) {
+                float y = 0.f;
 #pragma unroll
-          for (int w = 0; w < NWP; w++) y += s_part[w][lane];
-          ypart[(size_t)cc * m + r] = y;
+                for (int w = 0; w < NWP; w++) y += s_p4[w][tid];
+                ypart[(size_t)cc * m + row] = y;
+              }
+            }
+            __syncthreads();
+          }
         }
-        __syncthreads();
+      } else {
+        const int units = nslab * nch;
+        for (int u = g; u < units; u += G) {
+          const int sl = u % nslab, cc = u / nslab;
+          const int r = sl * HP_ROWS + lane, rr = r < m ? r : m - 1;
+          const int qa = q0 + cc * HP2_CW, qb = min(qa + HP2_CW, m);
+          constexpr int UB = HP2_CW / NWP;  // columns per warp (16)
+          S a[UB];
+#pragma unroll
+          for (int j = 0; j < UB; j++) {
+            const int q = qa + warp + NWP * j;
+            a[j] = q < qb ? A[rr + (size_t)q * lda] : S(0);
+          }
+          S acc0 = S(0), acc1 = S(0);
+#pragma unroll
+          for (int j = 0; j < UB; j += 2) {
+            const int q = qa + warp + NWP * j;
+            acc0 = fmac(a[j], q < qb ? sv[q] : S(0), acc0);
+            acc1 = fmac(a[j + 1], q + NWP < qb ? sv[q + NWP] : S(0), acc1);
+          }
+          s_part[warp][lane] = acc0 + acc1;
+          __syncthreads();
+          if (warp == 0 && r < m) {
+            S y = S(0);
+#pragma unroll
+            for (int w = 0; w < NWP; w++) y += s_part[w][lane];
+            ypart[(size_t)cc * m + r] = y;
+          }
+          __syncthreads();
+        }
       }
-      if (i > 0) {  // partials of V[:, :i]^H v over own rows (v = 0 above row c+1)
+      if (i > 0) {  // partials of V[:, :i]^H v over own rows
         if (tid < HESS_NB) s_acc[tid] = S(0);
         __syncthreads();
-        for (int sl = g; sl < nslab; sl += G) {
-          const int r = sl * HP_ROWS + lane;
+        for (int o = 0; o < nown; o++) {
+          const int r = (g + o * G) * HP_ROWS + lane;
+          const S vr = r < m ? sv[r] : S(0);
           for (int q = warp; q < i; q += NWP) {
-            S val = (r < m && r >= c + 1) ? conj(Vp[r + (size_t)q * ldv]) * sv[r] : S(0);
-            val = warp_sum(val);
+            S val = warp_sum(conj(VC(o, q)) * vr);
             if (lane == 0) s_acc[q] += val;
           }
         }
@@ -616,34 +695,49 @@ __global__ void __launch_bounds__(HP_TPB) hess_panel2_kernel(int m, S* A, int ld
         if (tid < HESS_NB) red2[g * HESS_NB + tid] = s_acc[tid];
       }
     }
+    HPROF(6);
     grid.sync();
+    HPROF(4);
     // ---- E ----
     {
       if (i > 0) cta_sum_partials<S>(red2, G, i, s_u, s_part);
+      else __syncthreads();
       const int nch = cdiv(m - (c + 1), HP2_CW);
-      const S ti = s_tau;
-      if (warp == 0)
-        for (int sl = g; sl < nslab; sl += G) {
-          const int r = sl * HP_ROWS + lane;
+      const S ti = s_tau, beta = s_beta;
+      for (int o = 0; o < nown; o++) {
+        const int r = (g + o * G) * HP_ROWS + lane;
+        S pa = S(0);
+        if (r < m)
+          for (int cc = warp; cc < nch; cc += NWP) pa += ypart[(size_t)cc * m + r];
+        s_part[warp][lane] = pa;
+        __syncthreads();
+        if (warp == 0) {
+          S y = S(0);
+#pragma unroll
+          for (int w = 0; w < NWP; w++) y += s_part[w][lane];
+          for (int q = 0; q < i; q++) y = y - YC(o, q) * s_u[q];
+          y = ti * y;
+          YC(o, i) = y;
           if (r < m) {
-            S y = S(0);
-            for (int cc = 0; cc < nch; cc++) y += ypart[(size_t)cc * m + r];
-            S t[HESS_NB];
-#pragma unroll
-            for (int q = 0; q < HESS_NB; q++) t[q] = q < i ? Y[r + (size_t)q * ldy] : S(0);
-#pragma unroll
-            for (int q = 0; q < HESS_NB; q++) y = y - t[q] * (q < i ? s_u[q] : S(0));
-            Y[r + (size_t)i * ldy] = ti * y;
+            Y[r + (size_t)i * ldy] = y;
+            if (r >= c + 1) ac[r] = (r == c + 1) ? beta : S(0);
           }
         }
-      if (g == 0 && tid < i) {
+        __syncthreads();
+      }
+      if (tid < i) {  // T[:, i] = -tau T u'  (every CTA keeps T; CTA 0 writes it out)
         S sum = S(0);
-        for (int q = tid; q < i; q++) sum = fmac(T[tid + q * ldt], s_u[q], sum);
-        T[tid + i * ldt] = -(ti * sum);
+        for (int q = tid; q < i; q++) sum = fmac(Tc[tid * HP2_LD + q], s_u[q], sum);
+        const S tv = -(ti * sum);
+        Tc[tid * HP2_LD + i] = tv;
+        if (g == 0) T[tid + i * ldt] = tv;
       }
       __syncthreads();
     }
+    HPROF(7);
   }
+#undef VC
+#undef YC
 }
 
 template <class S>
@@ -672,13 +766,17 @@ int hess2_grid(int m) {
   int dev, nsm, per = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = (size_t)m * sizeof(S);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(hess_panel2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = hess2_smem<S>(m);
+  if (smem > 200 * 1024) return 0;
+  // static + dynamic smem may pass 48 KB even when the dynamic part does not
+  if (cudaFuncSetAttribute(hess_panel2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hess_panel2_kernel<S>, HP_TPB, smem) != cudaSuccess)
     return 0;
   const int nslab = cdiv(m, HP_ROWS), units = nslab * cdiv(m, HP2_CW);
-  return std::min(per * nsm, std::max(nslab, std::min(units, nsm)));
+  const int G = std::min(per * nsm, std::max(nslab, std::min(units, nsm)));
+  return (G > 0 && cdiv(nslab, G) <= HP2_OWN) ? G : 0;  // each CTA caches at most HP2_OWN slabs
 }
 
 // grid size of the cooperative panel kernel (0 if it cannot be co-resident)
@@ -719,7 +817,8 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
       S* yp = w.part;
       void* args[] = {&mm, &Ap, &ldaa, &kk, &nb_, &Vv, &ldvv, &Yy, &ldyy, &Tt, &ldtt, &ta, &r1, &r2, &rR, &sl, &yp};
       const void* fn = hmode == 1 ? (const void*)hess_panel_coop_kernel<S> : (const void*)hess_panel2_kernel<S>;
-      MSY_CK(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(HP_TPB), args, (size_t)m * sizeof(S), st));
+      MSY_CK(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(HP_TPB), args,
+                                         hmode == 1 ? (size_t)m * sizeof(S) : hess2_smem<S>(m), st));
       MSY_LAUNCH_CK();
     }
     for (int i = 0; i < nbp && G == 0; i++) {
@@ -757,6 +856,17 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
       if (rc) return rc;
     }
   }
+#ifdef MSY_HESS_PROF
+  {
+    unsigned long long h[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_hess_prof, sizeof(h));
+    fprintf(stderr, "hess panel phases (ms, CTA 0): A %.2f syncA %.2f B %.2f syncs %.2f C %.2f D %.2f E %.2f\n",
+            h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6, h[6] * 1e-6, h[7] * 1e-6);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_hess_prof, z, sizeof(z));
+  }
+#endif
   clear_below_sub_kernel<S><<<dim3(cdiv(m, 256), m), 256, 0, st>>>(m, A, lda);
   MSY_LAUNCH_CK();
   // ---- form Q0 = P_0 ... P_{m-3} by backward panel accumulation ----
