@@ -178,6 +178,55 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+KCLASSES = ["gemm_dmma_kernel (fp64 DMMA.8x8x4)", "gemm_simt_kernel (fp32/complex FFMA)",
+            "apply_z_kernel (window Z application, FFMA)", "chase_kernel (bulge chase, one CTA per chain)",
+            "trsyl_step_kernel", "hess_panel kernel", "schur_small/mss (one-CTA Schur)", "aed_kernel"]
+KPEAK = {0: "dmma", 1: "ffma", 2: "ffma"}
+
+
+def ktimer(L, op):
+    n = len(KCLASSES)
+    cnt, ms, fl = (ct.c_longlong * n)(), (ct.c_double * n)(), (ct.c_double * n)()
+    L.sylv_ktimer(op, n, cnt, ms, fl)
+    return [(cnt[i], ms[i], fl[i]) for i in range(n)]
+
+
+def kernel_rooflines(rows, pk, steps):
+    """Per kernel class: launches, event-timed ms per step, share of the summed kernel time, achieved
+    TFLOP/s from the algorithmic flops declared at each launch.  roofline = the dominant class that
+    has an algorithmic flop count."""
+    tot = sum(r[1] for r in rows) or 1.0
+    out = {}
+    for i, (c, ms, fl) in enumerate(rows):
+        if c == 0:
+            continue
+        e = {"launches_per_step": c / steps, "ms_per_step": ms / steps, "share": ms / tot}
+        if fl > 0 and ms > 0:
+            e["tflops"] = fl / (ms * 1e-3) / 1e12
+            pkv = pk.get(KPEAK.get(i))
+            if pkv:
+                e["frac_of_peak"] = e["tflops"] / pkv
+        out[KCLASSES[i]] = e
+    best = None
+    for i, (c, ms, fl) in enumerate(rows):
+        if c and fl > 0 and ms > 0 and (best is None or ms > rows[best][1]):
+            best = i
+    roof = None
+    if best is not None:
+        c, ms, fl = rows[best]
+        ach = fl / (ms * 1e-3) / 1e12
+        peak = pk.get(KPEAK.get(best))
+        roof = {"bound": "tensor" if best == 0 else "fp32-simt", "kernel": KCLASSES[best], "achieved": ach,
+                "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if peak else None, "traffic": None,
+                "share_of_kernel_time": ms / tot,
+                "peak_source": ("measured live by sylv_microbench (DMMA.8x8x4 / FFMA loops); MEASURED_PEAKS.json "
+                                "has no fp32/fp64 figure"),
+                "algorithmic": (f"{fl / c:.3e} flop per launch (flops declared at each launch from its shapes), "
+                                f"{ms / c:.3f} ms average launch, {c / steps:.0f} launches per step, CUDA events "
+                                f"on the launching stream over the timed region")}
+    return roof, out
+
+
 def dmma_roofline(L, st, dev, m):
     """Live roofline of the dominant kernel class: the fp64 DMMA GEMM engine (CUDA events on its stream)."""
     import torch
@@ -269,6 +318,7 @@ def run_ours(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     reps = []
     launches0 = L.sylv_launch_count()
+    ktimer(L, 1)
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.fill_(float(i))
@@ -277,6 +327,8 @@ def run_ours(args):
             evs[i][1].record(st)
             reps.append(rep)
         torch.cuda.synchronize(dev)
+    krows = ktimer(L, 2)
+    ktimer(L, 0)
     launches = (L.sylv_launch_count() - launches0) // max(1, args.steps)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
@@ -317,9 +369,14 @@ def run_ours(args):
         e2e = {"value": world * ne / (tot / 1e3), "unit": "solves/s",
                "h2d_bytes_per_step": (m * m + n * n + m * n) * esz, "d2h_bytes_per_step": m * n * esz}
     # ---- roofline: the fp64 DMMA GEMM engine of the contraction phases, timed live ----
-    roof = sol_roof = None
+    roof = sol_roof = kern = gemm_roof = None
     if rank == 0:
-        roof, pk = dmma_roofline(L, st, dev, m)
+        gemm_roof, pk = dmma_roofline(L, st, dev, m)
+        roof, kern = kernel_rooflines(krows, pk, args.steps)
+        dm = kern.get(KCLASSES[0])
+        if dm and "tflops" in dm:  # the north star's "FP64 tensor peak in its GEMM phases", live in the step
+            gemm_roof["in_step"] = {"tflops": dm["tflops"], "frac": dm.get("frac_of_peak"),
+                                    "ms_per_step": dm["ms_per_step"]}
         sol_roof = solve_roofline(pk, args.variant, pr.kind, m, n, k, cx, total_ms / args.steps / 1e3, 1)
         sol_roof["phase_ms"] = {"schur": reps[-1].ms_schur, "orth": reps[-1].ms_orth, "setup": reps[-1].ms_setup,
                                 "y0": reps[-1].ms_y0, "refine": reps[-1].ms_refine, "recover": reps[-1].ms_recover}
@@ -343,7 +400,8 @@ def run_ours(args):
                        "residual": reps[-1].residual,
                        "schur_sweeps": [reps[-1].schur_sweeps_a, reps[-1].schur_sweeps_b],
                        "parallelism": f"replicas x{world}"},
-            "roofline": roof, "solve_roofline": sol_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "gemm_phase_roofline": gemm_roof, "kernels": kern, "solve_roofline": sol_roof,
+            "cpu_baseline": cpu, "e2e": e2e,
             "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
             "gpu_launches": int(launches),
             "measured_peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},

@@ -95,6 +95,12 @@ unsigned long long sylv_launch_count(void);
 /* measured arithmetic peak in TFLOP/s: kind 0 = FP32 FFMA, 1 = FP64 DFMA,
  * 2 = FP64 DMMA.8x8x4 (the roofline denominators of the path) */
 int sylv_microbench(int kind, double* tflops, void* stream);
+/* live kernel-class timer (bench roofline evidence): op 1 = clear + enable,
+ * op 0 = disable, op 2 = read and clear.  Classes: 0 fp64 DMMA GEMM, 1 SIMT GEMM,
+ * 2 Z application, 3 bulge chase, 4 trsyl step, 5 Hessenberg panel, 6 one-CTA
+ * Schur, 7 AED.  On read, per class (arrays of ncls entries): launches, summed
+ * event-interval milliseconds, summed algorithmic flops declared at the launch. */
+int sylv_ktimer(int op, int ncls, long long* launches, double* ms, double* flops);
 
 /* mp_orth / mp_inv (refinement.py:205-297): A m x m, B n x n, C and X m x n,
  * fp64 (complex_data = 0) or complex128 (complex_data = 1). */

@@ -25,7 +25,7 @@ MAX_NORMS = 256
 DTYPE = {"float32": 0, "float64": 1, "complex64": 2, "complex128": 3}
 
 EXPORTS = (
-    "sylv_version", "sylv_status_string", "sylv_launch_count", "sylv_microbench",
+    "sylv_version", "sylv_status_string", "sylv_launch_count", "sylv_microbench", "sylv_ktimer",
     "sylv_workspace_size", "sylv_solve", "sylv_batched_workspace_size", "sylv_solve_batched",
     "sylv_refine_workspace_size", "sylv_refine", "sylv_schur_workspace_size", "sylv_schur",
     "sylv_trsyl_workspace_size", "sylv_trsyl", "sylv_orth_workspace_size", "sylv_orth", "sylv_gemm",
@@ -73,6 +73,7 @@ def lib():
         L.sylv_status_string.argtypes = [ip]
         L.sylv_launch_count.restype = ct.c_ulonglong
         L.sylv_microbench.argtypes = [ip, ct.POINTER(ct.c_double), vp]
+        L.sylv_ktimer.argtypes = [ip, ip, ct.POINTER(ct.c_longlong), ct.POINTER(ct.c_double), ct.POINTER(ct.c_double)]
         L.sylv_workspace_size.argtypes = [ct.POINTER(Params), ct.POINTER(sz)]
         L.sylv_solve.argtypes = [ct.POINTER(Params), vp, ip, vp, ip, vp, ip, vp, ip, vp, sz, vp,
                                  ct.POINTER(Report)]

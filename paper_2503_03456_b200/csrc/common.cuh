@@ -6,6 +6,8 @@
 // 2 = complex<float> (c), 3 = complex<double> (z).
 #pragma once
 #include <atomic>
+#include <mutex>
+#include <vector>
 #include <cstring>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -227,6 +229,52 @@ inline cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st
   memcpy(dst, pinned, bytes);
   return cudaSuccess;
 }
+
+// ---- live per-kernel-class timing (the bench's roofline evidence) ------------
+// When enabled (sylv_ktimer), every launch of an instrumented class is bracketed by
+// two CUDA events on its own stream; reading sums the event intervals and the
+// algorithmic flops declared at the launch site.
+enum KClass { KC_DMMA = 0, KC_SIMT, KC_APPLYZ, KC_CHASE, KC_TRSYL, KC_HESS, KC_SMALL, KC_AED, KC_N };
+struct KTimer {
+  struct Rec { int cls; double flops; cudaEvent_t a, b; };
+  std::atomic<int> on{0};
+  std::mutex mu;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {  // under mu
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+inline KTimer& ktimer() {
+  static KTimer t;
+  return t;
+}
+struct KScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  int cls;
+  double flops;
+  KScope(int c, double f, cudaStream_t s) : st(s), cls(c), flops(f) {
+    KTimer& t = ktimer();
+    if (!t.on.load(std::memory_order_relaxed)) return;
+    {
+      std::lock_guard<std::mutex> g(t.mu);
+      a = t.get();
+      b = t.get();
+    }
+    cudaEventRecord(a, st);
+  }
+  ~KScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    KTimer& t = ktimer();
+    std::lock_guard<std::mutex> g(t.mu);
+    t.recs.push_back({cls, flops, a, b});
+  }
+};
 
 // one-time kernel attribute setup, safe under concurrent first calls
 #define MSY_SMEM_ATTR_ONCE(kern, bytes)                                                             \

@@ -146,6 +146,7 @@ static int gemm_simt_launch(int M, int N, int K, S alpha, const S* A, int lda, c
                             int ldc, cudaStream_t st) {
   typedef GemmCfg<S> G;
   dim3 grid(cdiv(M, G::BM), cdiv(N, G::BN));
+  KScope ks(KC_SIMT, (tr<S>::cx ? 8.0 : 2.0) * M * N * K, st);
   gemm_simt_kernel<S, OPA, OPB><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, K, nullptr);
   MSY_LAUNCH_CK();
   return 0;
@@ -171,6 +172,7 @@ static int gemm_splitk_launch(int M, int N, int K, S alpha, const S* A, int lda,
   const int kchunk = cdiv(cdiv(K, splits), G::BK) * G::BK;
   splits = cdiv(K, kchunk);
   dim3 grid(cdiv(M, G::BM), cdiv(N, G::BN), splits);
+  KScope ks(KC_SIMT, (tr<S>::cx ? 8.0 : 2.0) * M * N * K, st);
   gemm_simt_kernel<S, OPA, OPB><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ws);
   MSY_LAUNCH_CK();
   splitk_reduce_kernel<S><<<dim3(cdiv(M, 128), N), 128, 0, st>>>(M, N, splits, ws, alpha, beta, C, ldc);

@@ -132,6 +132,7 @@ inline int gemm_dmma_try<double>(char opa, char opb, int M, int N, int K, double
   dim3 grid(cdiv(M, DM_BM), cdiv(N, DM_BN));
 #define MSY_D(a, b)                                                                                      \
   if (opa == a && opb == b) {                                                                            \
+    KScope ks__(KC_DMMA, 2.0 * M * N * K, st);                                                           \
     gemm_dmma_kernel<a, b><<<grid, 128, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);          \
     MSY_LAUNCH_CK();                                                                                     \
     return 0;                                                                                            \

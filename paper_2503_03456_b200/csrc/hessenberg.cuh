@@ -817,6 +817,7 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
       S* yp = w.part;
       void* args[] = {&mm, &Ap, &ldaa, &kk, &nb_, &Vv, &ldvv, &Yy, &ldyy, &Tt, &ldtt, &ta, &r1, &r2, &rR, &sl, &yp};
       const void* fn = hmode == 1 ? (const void*)hess_panel_coop_kernel<S> : (const void*)hess_panel2_kernel<S>;
+      KScope ks(KC_HESS, 0, st);
       MSY_CK(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(HP_TPB), args,
                                          hmode == 1 ? (size_t)m * sizeof(S) : hess2_smem<S>(m), st));
       MSY_LAUNCH_CK();

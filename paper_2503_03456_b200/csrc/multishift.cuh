@@ -227,6 +227,15 @@ struct ApplyJobs {
   int start[KMAX + 1], nz[KMAX], r0[KMAX], cL0[KMAX], cL1[KMAX], rlo[KMAX], rR1[KMAX], mU[KMAX];
   const S* Z[KMAX];
 };
+// algorithmic flops of one apply_z_multi launch
+template <class S>
+double applyz_flops(const ApplyJobs<S>& j) {
+  double f = 0;
+  for (int i = 0; i < j.n; i++)
+    f += (double)j.nz[i] * j.nz[i] * ((j.cL1[i] > j.cL0[i] ? j.cL1[i] - j.cL0[i] : 0) +
+                                      (j.rR1[i] > j.rlo[i] ? j.rR1[i] - j.rlo[i] : 0) + j.mU[i]);
+  return (tr<S>::cx ? 8.0 : 2.0) * f;
+}
 template <class S>
 __global__ void __launch_bounds__(256) apply_z_multi_kernel(S* H, int ldh, S* U, int ldu, const ApplyJobs<S> jobs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -250,6 +259,7 @@ int apply_z_regions(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int
   if (nz > MsCfg<S>::W) return -4;
   int nblk = (cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
   if (nblk == 0) return 0;
+  KScope ks(KC_APPLYZ, (tr<S>::cx ? 8.0 : 2.0) * nz * nz * ((cL1 > cL0 ? cL1 - cL0 : 0) + rR1 + (U ? m : 0)), st);
   apply_z_kernel<S><<<nblk, 256, applyz_smem<S>(nz), st>>>(nz, Z, H, ldh, w0, cL0, cL1, rR1, U, ldu, U ? m : 0);
   MSY_LAUNCH_CK();
   return 0;

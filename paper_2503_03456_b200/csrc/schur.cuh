@@ -12,6 +12,7 @@
 #include "multishift.cuh"
 #include "schur_small.cuh"
 #include "schur_mss.cuh"
+#include "aed.cuh"
 
 #include <chrono>
 #include <cstdlib>
@@ -28,6 +29,7 @@ struct SchurWs {
   R* wi;
   R* shifts;  // 4 per bulge
   int* dinfo; // small device ints
+  S* vaed;    // AED window Schur vectors
   static void carve(Arena& ar, int m, SchurWs& w) {
     if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
     w.Z = ar.get<S>((size_t)2 * KMAX * ZMAX * ZMAX);
@@ -36,12 +38,15 @@ struct SchurWs {
     w.wi = ar.get<R>(256);
     w.shifts = ar.get<R>(4 * 128);
     w.dinfo = ar.get<int>(64);
+    w.vaed = m > SmallCfg<S>::NMAX ? ar.get<S>((size_t)AedCfg<S>::NW * AedCfg<S>::NW) : nullptr;
   }
 };
 
 struct SchurStats {
   int status, sweeps, small_calls, windows;
   double ms_hess, ms_scan, ms_small, ms_shift, ms_sweep;  // filled when MSY_SCHUR_TIMING=1
+  int aed_calls, aed_deflated, ms_sweeps;                  // AED windows, eigenvalues they deflated, QR sweeps
+  double ms_aed;
 };
 
 // diagnostic phase timer: synchronises the stream at each mark (only when enabled)
@@ -192,8 +197,11 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
                                cdiv(jc[f].mU[j], 32);
         }
       }
-      chase_kernel<S><<<nj, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
-      MSY_LAUNCH_CK();
+      {
+        KScope ks(KC_CHASE, 0, st);
+        chase_kernel<S><<<nj, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
+        MSY_LAUNCH_CK();
+      }
       if (ovl && tau > 0) MSY_CK(cudaStreamWaitEvent(st, sc->evD, 0));  // far(tau-1) done
       for (int f = 0; f < 2; f++) {
         cudaStream_t s2 = f == 0 ? st : fst;
@@ -202,10 +210,12 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
           MSY_CK(cudaStreamWaitEvent(fst, sc->evN, 0));
         }
         if (jr[f].start[nj] > 0) {
+          KScope ks(KC_APPLYZ, applyz_flops<S>(jr[f]), s2);
           apply_z_multi_kernel<S><<<jr[f].start[nj], 256, applyz_smem<S>(W), s2>>>(H, ldh, U, ldu, jr[f]);
           MSY_LAUNCH_CK();
         }
         if (jc[f].start[nj] > 0) {
+          KScope ks(KC_APPLYZ, applyz_flops<S>(jc[f]), s2);
           apply_z_multi_kernel<S><<<jc[f].start[nj], 256, applyz_smem<S>(W), s2>>>(H, ldh, U, ldu, jc[f]);
           MSY_LAUNCH_CK();
         }
@@ -222,8 +232,11 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
     cj.ws[0] = w.ws; cj.we[0] = w.we; cj.t0[0] = w.t0; cj.t1[0] = w.t1;
     cj.shifts[0] = shifts;
     cj.Z[0] = Zbuf + (k & 1) * ZMAX * ZMAX;
-    chase_kernel<S><<<1, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
-    MSY_LAUNCH_CK();
+    {
+      KScope ks(KC_CHASE, 0, st);
+      chase_kernel<S><<<1, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
+      MSY_LAUNCH_CK();
+    }
     if (sc->aux) MSY_CK(cudaEventRecord(sc->evC, st));
     return 0;
   };
@@ -269,7 +282,7 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
   if (!sc) sc = sweep_ctx();
   typedef typename tr<S>::R R;
   constexpr int NMIN = SmallCfg<S>::NMAX;
-  SchurStats loc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  SchurStats loc = {};
   if (m <= NMIN) {
     int rc = schur_small_launch<S>(m, A, lda, U, ldu, SS_HESS | SS_WANTZ, nullptr, nullptr, w.dinfo, st);
     if (rc) return rc;
@@ -320,15 +333,69 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
       continue;
     }
     if (loc.sweeps >= limit) { loc.status = ST_ITERLIMIT; break; }
-    int nb = std::min(MsCfg<S>::NB, std::max(1, (sz - 8) / 8));
+    static const int kmax_env = getenv("MSY_CHAINS") ? atoi(getenv("MSY_CHAINS")) : KMAX;
+    bool exc = (stag > 0 && stag % 6 == 0);
+    // ---- aggressive early deflation on the trailing window (aed.cuh) ----
+    static const int aed_on = getenv("MSY_AED") ? atoi(getenv("MSY_AED")) : 0;
+    static const int aed_nw = getenv("MSY_AED_NW") ? atoi(getenv("MSY_AED_NW")) : AedCfg<S>::NW;
+    static const int aed_gmax = getenv("MSY_AED_GMAX") ? atoi(getenv("MSY_AED_GMAX")) : 16;
+    static const int aed_nibble = getenv("MSY_AED_NIBBLE") ? atoi(getenv("MSY_AED_NIBBLE")) : 14;
+    int aed_ls = 0;
+    if (aed_on && !exc) {
+      const int nw = std::max(16, std::min({aed_nw, AedCfg<S>::NW, sz - 1}));
+      const int kwtop = hi - nw + 1;
+      const S* src = A + kwtop + (size_t)kwtop * lda;
+      copy_block_kernel<S><<<dim3(cdiv(nw, 128), nw), 128, 0, st>>>(nw, src, lda, w.sblk, nw);
+      MSY_LAUNCH_CK();
+      rc = schur_small_launch<S>(nw, w.sblk, nw, w.vaed, nw, SS_WANTZ, nullptr, nullptr, w.dinfo + 32, st);
+      if (rc) return rc;
+      MSY_SMEM_ATTR_ONCE(aed_kernel<S>, (int)aed_smem_bytes<S>());
+      KScope ks(KC_AED, 0, st);
+      aed_kernel<S><<<1, AED_THREADS, aed_smem_bytes<S>(), st>>>(nw, w.sblk, w.vaed, A, lda, kwtop, lo, w.wr, w.wi,
+                                                                 w.dinfo + 40, aed_gmax, w.dinfo + 32);
+      MSY_LAUNCH_CK();
+      int ainfo[12];
+      MSY_CK(d2h(ainfo, w.dinfo + 32, 12 * sizeof(int), st));
+      const int nd = ainfo[8];
+      aed_ls = ainfo[9];
+      loc.aed_calls++;
+      loc.aed_deflated += nd;
+      if (nd > 0) {
+        rc = apply_z<S>(m, nw, w.vaed, A, lda, U, ldu, kwtop, st);
+        if (rc) return rc;
+      }
+      pt.lap(&loc.ms_aed);
+      if (nd > 0 && 100 * nd > aed_nibble * nw) continue;  // enough deflated: re-examine before sweeping
+      if (nd > 0) {
+        hi -= nd;
+        last_hi = hi;
+        stag = 0;
+        sz = hi - lo + 1;
+        if (sz <= NMIN) continue;
+      }
+    }
+    int nb, K = 1, ns;
+    if (aed_ls >= 8) {  // shifts: the undeflated window eigenvalues, bottom-most first
+      const int npairs = aed_ls / 2 - 1;
+      nb = std::min({MsCfg<S>::NB, npairs, std::max(1, (sz - 8) / 8)});
+      if (nb == MsCfg<S>::NB && kmax_env > 1)
+        K = std::max(1, std::min({std::min(kmax_env, KMAX), npairs / nb, sz / (12 * nb)}));
+      pair_shifts_kernel<S><<<1, 32, 0, st>>>(aed_ls, w.wr, w.wi, nb * K, w.shifts, 0, A, lda, lo, hi, w.dinfo + 24);
+      MSY_LAUNCH_CK();
+      pt.lap(&loc.ms_shift);
+      rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, K, w.shifts, w.Z, st, &loc.windows, sc);
+      if (rc) return rc;
+      pt.lap(&loc.ms_sweep);
+      loc.sweeps++;
+      loc.ms_sweeps++;
+      continue;
+    }
+    nb = std::min(MsCfg<S>::NB, std::max(1, (sz - 8) / 8));
     // several chains per sweep when the active block is large and the trailing
     // block that supplies their shifts fits the one-CTA kernel
-    int K = 1;
-    static const int kmax_env = getenv("MSY_CHAINS") ? atoi(getenv("MSY_CHAINS")) : KMAX;
     if (nb == MsCfg<S>::NB && kmax_env > 1)
       K = std::max(1, std::min({std::min(kmax_env, KMAX), EigCfg<S>::NMAX / (2 * nb), sz / (12 * nb)}));
-    int ns = 2 * nb * K;
-    bool exc = (stag > 0 && stag % 6 == 0);
+    ns = 2 * nb * K;
     if (!exc) {
       const S* src = A + (hi - ns + 1) + (size_t)(hi - ns + 1) * lda;
       copy_block_kernel<S><<<dim3(cdiv(ns, 128), ns), 128, 0, st>>>(ns, src, lda, w.sblk, ns);
@@ -348,6 +415,7 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     if (rc) return rc;
     pt.lap(&loc.ms_sweep);
     loc.sweeps++;
+    loc.ms_sweeps++;
   }
   if (stats) *stats = loc;
   return 0;

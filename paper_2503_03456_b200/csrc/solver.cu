@@ -495,6 +495,30 @@ int sylv_microbench(int kind, double* tflops, void* stream) {
   return msy::microbench(kind, tflops, (cudaStream_t)stream);
 }
 
+int sylv_ktimer(int op, int ncls, long long* launches, double* ms, double* flops) {
+  msy::KTimer& t = msy::ktimer();
+  if (op == 0 || op == 1) {
+    t.on.store(0);
+    std::lock_guard<std::mutex> g(t.mu);
+    for (auto& r : t.recs) { t.pool.push_back(r.a); t.pool.push_back(r.b); }
+    t.recs.clear();
+    if (op == 1) t.on.store(1);
+    return SYLV_OK;
+  }
+  if (op != 2 || ncls < 0) return SYLV_EINVAL;
+  std::lock_guard<std::mutex> g(t.mu);
+  for (int c = 0; c < ncls; c++) { launches[c] = 0; ms[c] = 0; flops[c] = 0; }
+  for (auto& r : t.recs) {
+    float e = 0;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess) e = 0;
+    if (r.cls < ncls) { launches[r.cls]++; ms[r.cls] += e; flops[r.cls] += r.flops; }
+    t.pool.push_back(r.a);
+    t.pool.push_back(r.b);
+  }
+  t.recs.clear();
+  return SYLV_OK;
+}
+
 const char* sylv_status_string(int s) {
   switch (s) {
     case SYLV_OK: return "ok";
@@ -798,8 +822,11 @@ static int schur_entry(int m, void* A, int lda, void* U, int ldu, void* ws, size
   MSY_CK(host_sync(st));
   if (info) { info[0] = s.status; info[1] = s.sweeps; info[2] = s.small_calls; info[3] = s.windows; }
   if (getenv("MSY_SCHUR_TIMING"))
-    fprintf(stderr, "schur m=%d: hess %.1f ms, scan %.1f, small %.1f, shift %.1f, sweep %.1f\n", m, s.ms_hess,
-            s.ms_scan, s.ms_small, s.ms_shift, s.ms_sweep);
+    fprintf(stderr,
+            "schur m=%d: hess %.1f ms, scan %.1f, small %.1f, shift %.1f, sweep %.1f, aed %.1f | qr sweeps %d, "
+            "aed windows %d deflating %d\n",
+            m, s.ms_hess, s.ms_scan, s.ms_small, s.ms_shift, s.ms_sweep, s.ms_aed, s.ms_sweeps, s.aed_calls,
+            s.aed_deflated);
   return 0;
 }
 int sylv_schur(int dtype, int m, void* A, int lda, void* U, int ldu, void* ws, size_t ws_bytes, void* stream,

@@ -421,6 +421,7 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
       cnt += (long)std::min(d, nbj) * std::max(0, nbi - d);
     }
     if (cnt == 0) continue;
+    KScope ks(KC_TRSYL, 0, st);
     trsyl_step_kernel<S><<<(unsigned)cnt, TRS_TPB, trsyl_smem<S>(), st>>>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb, w.cb,
                                                                       nbi, nbj, d, status);
     MSY_LAUNCH_CK();
