@@ -138,6 +138,111 @@ __host__ __device__ bool block_swap_q(const D* M, int p, int q, D* Q, double tol
   return ll <= tol * fmax(mn, R(1e-300));
 }
 
+// Deflation check of a window in Schur form (one warp; T, V in smem with stride LD;
+// Qs: 16 smem scratch entries, okf: smem flag).  Candidates are tested from the
+// bottom; an undeflatable block joins a group kept at the bottom of the undeflated
+// part, and each later candidate is swapped below that group before its test.
+// Returns ns, the number of undeflated leading rows (the deflated blocks occupy
+// [ns, nw)).  s == 0 deflates everything.
+template <class S, int LD>
+__device__ int aed_deflate_warp(S* T, S* V, int nw, S s, int gmax, int lane, S* Qs, int* okf) {
+  typedef typename tr<S>::R R;
+  typedef typename wide<S>::T D;
+  const R u = tr<S>::u();
+#define TT(i, j) T[(i) + (j) * LD]
+#define VV(i, j) V[(i) + (j) * LD]
+  int ns = nw, g = 0;
+  bool stop = iszero(s);  // s == 0: everything deflates
+  if (stop) ns = 0;
+  while (!stop && ns - g > 0) {
+    const int e = ns - g - 1;
+    const int b = (!tr<S>::cx && e > 0 && !iszero(TT(e, e - 1))) ? 2 : 1;
+    int pos = e - b + 1;
+    // swap the candidate below the undeflatable group
+    bool ok = true;
+    while (pos + b < ns) {
+      const int nxt = pos + b;
+      const int q = (!tr<S>::cx && nxt + 1 < ns && !iszero(TT(nxt + 1, nxt))) ? 2 : 1;
+      const int k = b + q;
+      if (lane == 0) {
+        D M[16], Q[16];
+        for (int i = 0; i < 16; i++) M[i] = D(0);
+        for (int j = 0; j < k; j++)
+          for (int i = 0; i < k; i++) M[i + 4 * j] = conv<D>(TT(pos + i, pos + j));
+        const bool good = block_swap_q<D>(M, b, q, Q, 64.0 * (double)u);
+        (*okf) = good;
+        for (int j = 0; j < 4; j++)
+          for (int i = 0; i < 4; i++) Qs[i + 4 * j] = conv<S>(Q[i + 4 * j]);
+      }
+      __syncwarp();
+      if (!(*okf)) { ok = false; break; }
+      S qv[16];
+#pragma unroll
+      for (int i = 0; i < 16; i++) qv[i] = Qs[i];
+      // rows pos..pos+k-1 of T, columns pos..nw-1: Q^H (.)
+      for (int c = pos + lane; c < nw; c += 32) {
+        S t[4], o[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) t[i] = i < k ? TT(pos + i, c) : S(0);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          S a = S(0);
+#pragma unroll
+          for (int l = 0; l < 4; l++) a = fmacc(qv[l + 4 * i], t[l], a);
+          o[i] = a;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if (i < k) TT(pos + i, c) = o[i];
+      }
+      __syncwarp();
+      // columns pos..pos+k-1 of T (rows 0..pos+k-1) and of V (all rows): (.) Q
+      for (int e2 = lane; e2 < (pos + k) + nw; e2 += 32) {
+        S* Mx = e2 < pos + k ? T : V;
+        const int r = e2 < pos + k ? e2 : e2 - pos - k;
+        S t[4], o[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) t[i] = i < k ? Mx[r + (pos + i) * LD] : S(0);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          S a = S(0);
+#pragma unroll
+          for (int l = 0; l < 4; l++) a = fmac(t[l], qv[l + 4 * i], a);
+          o[i] = a;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if (i < k) Mx[r + (pos + i) * LD] = o[i];
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int r = pos + q; r < pos + k; r++)
+          for (int c = pos; c < pos + q; c++) TT(r, c) = S(0);
+      __syncwarp();
+      pos += q;
+    }
+    if (!ok) break;
+    // candidate now occupies [ns - b, ns)
+    const int bt = ns - 1;
+    R foo = absv(TT(bt, bt));
+    R sp = absv(s * conj(VV(0, bt)));
+    if (b == 2) {
+      foo += sqrt(absv(TT(bt, bt - 1))) * sqrt(absv(TT(bt - 1, bt)));
+      sp = fmax(sp, absv(s * conj(VV(0, bt - 1))));
+    }
+    if (foo == R(0)) foo = absv(s);
+    if (sp <= fmax(R(1e-30), u * foo)) {
+      ns -= b;
+    } else {
+      g += b;
+      if (g >= gmax) stop = true;
+    }
+  }
+  return ns;
+#undef TT
+#undef VV
+}
+
 template <class S> struct AedCfg { static constexpr int NW = SmallCfg<S>::NMAX; };
 constexpr int AED_THREADS = 256;
 
@@ -208,93 +313,7 @@ __global__ void __launch_bounds__(AED_THREADS) aed_kernel(int nw, const S* Tg, S
 #define VV(i, j) V[(i) + (j) * LD]
   // ---------------- deflation check (warp 0) --------------------------------
   if (warp == 0) {
-    int ns = nw, g = 0;
-    bool stop = iszero(s);  // s == 0: everything deflates
-    if (stop) ns = 0;
-    while (!stop && ns - g > 0) {
-      const int e = ns - g - 1;
-      const int b = (!tr<S>::cx && e > 0 && !iszero(TT(e, e - 1))) ? 2 : 1;
-      int pos = e - b + 1;
-      // swap the candidate below the undeflatable group
-      bool ok = true;
-      while (pos + b < ns) {
-        const int nxt = pos + b;
-        const int q = (!tr<S>::cx && nxt + 1 < ns && !iszero(TT(nxt + 1, nxt))) ? 2 : 1;
-        const int k = b + q;
-        if (lane == 0) {
-          D M[16], Q[16];
-          for (int i = 0; i < 16; i++) M[i] = D(0);
-          for (int j = 0; j < k; j++)
-            for (int i = 0; i < k; i++) M[i + 4 * j] = conv<D>(TT(pos + i, pos + j));
-          const bool good = block_swap_q<D>(M, b, q, Q, 64.0 * (double)u);
-          sh_ok = good;
-          for (int j = 0; j < 4; j++)
-            for (int i = 0; i < 4; i++) Qs[i + 4 * j] = conv<S>(Q[i + 4 * j]);
-        }
-        __syncwarp();
-        if (!sh_ok) { ok = false; break; }
-        S qv[16];
-#pragma unroll
-        for (int i = 0; i < 16; i++) qv[i] = Qs[i];
-        // rows pos..pos+k-1 of T, columns pos..nw-1: Q^H (.)
-        for (int c = pos + lane; c < nw; c += 32) {
-          S t[4], o[4];
-#pragma unroll
-          for (int i = 0; i < 4; i++) t[i] = i < k ? TT(pos + i, c) : S(0);
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            S a = S(0);
-#pragma unroll
-            for (int l = 0; l < 4; l++) a = fmacc(qv[l + 4 * i], t[l], a);
-            o[i] = a;
-          }
-#pragma unroll
-          for (int i = 0; i < 4; i++)
-            if (i < k) TT(pos + i, c) = o[i];
-        }
-        __syncwarp();
-        // columns pos..pos+k-1 of T (rows 0..pos+k-1) and of V (all rows): (.) Q
-        for (int e2 = lane; e2 < (pos + k) + nw; e2 += 32) {
-          S* Mx = e2 < pos + k ? T : V;
-          const int r = e2 < pos + k ? e2 : e2 - pos - k;
-          S t[4], o[4];
-#pragma unroll
-          for (int i = 0; i < 4; i++) t[i] = i < k ? Mx[r + (pos + i) * LD] : S(0);
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            S a = S(0);
-#pragma unroll
-            for (int l = 0; l < 4; l++) a = fmac(t[l], qv[l + 4 * i], a);
-            o[i] = a;
-          }
-#pragma unroll
-          for (int i = 0; i < 4; i++)
-            if (i < k) Mx[r + (pos + i) * LD] = o[i];
-        }
-        __syncwarp();
-        if (lane == 0)
-          for (int r = pos + q; r < pos + k; r++)
-            for (int c = pos; c < pos + q; c++) TT(r, c) = S(0);
-        __syncwarp();
-        pos += q;
-      }
-      if (!ok) break;
-      // candidate now occupies [ns - b, ns)
-      const int bt = ns - 1;
-      R foo = absv(TT(bt, bt));
-      R sp = absv(s * conj(VV(0, bt)));
-      if (b == 2) {
-        foo += sqrt(absv(TT(bt, bt - 1))) * sqrt(absv(TT(bt - 1, bt)));
-        sp = fmax(sp, absv(s * conj(VV(0, bt - 1))));
-      }
-      if (foo == R(0)) foo = absv(s);
-      if (sp <= fmax(R(1e-30), u * foo)) {
-        ns -= b;
-      } else {
-        g += b;
-        if (g >= gmax) stop = true;
-      }
-    }
+    const int ns = aed_deflate_warp<S, LD>(T, V, nw, s, gmax, lane, Qs, &sh_ok);
     if (lane == 0) sh_ns = ns;
   }
   __syncthreads();
