@@ -50,7 +50,10 @@ enum {
 };
 
 enum { SYLV_KIND_GENERAL = 0, SYLV_KIND_LYAPUNOV = 1 };
-enum { SYLV_VARIANT_ORTH = 0, SYLV_VARIANT_INV = 1 };
+/* SYLV_VARIANT_BS: the fp64 Bartels-Stewart comparator (sylvester.py:160-178):
+ * Schur in binary64 (low_bits must be 64), F = U_A^H C U_B, one triangular solve,
+ * X = U_A Y U_B^H; no refinement (iterations = 0). */
+enum { SYLV_VARIANT_ORTH = 0, SYLV_VARIANT_INV = 1, SYLV_VARIANT_BS = 2 };
 /* where a typed failure happened: inside a refinement correction solve, at the
  * initial (u_l) triangular solve, or as a non-finite iterate after an update */
 enum { SYLV_STAGE_REFINEMENT = 0, SYLV_STAGE_INITIAL = 1, SYLV_STAGE_DIVERGED = 2 };

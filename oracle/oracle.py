@@ -219,3 +219,19 @@ def mp_solve(A, B, C, variant="orth", ul="binary32", kind="general", eps=None, m
     if rc:
         raise OracleError(rc)
     return _report_dict(rep, X)
+
+
+def bartels_stewart(A, B, C, kind="general", f32=False):
+    """bartels_stewart (sylvester.py:160-178) composed from the restated kernels: Schur of A
+    (and of B, or T_B = T_A^H, U_B = U_A for Lyapunov), Ct = (U_A^H C) U_B, the triangular
+    solve, X = (U_A Y) U_B^H.  Returns (X, residual)."""
+    A, B, C = _c(A), _c(B), _c(C)
+    UA, TA, _ = schur(A, f32)
+    if kind == "lyapunov":
+        UB, TB = UA, np.ascontiguousarray(TA.conj().T)
+    else:
+        UB, TB, _ = schur(B, f32)
+    Ct = gemm(1.0, gemm(1.0, np.ascontiguousarray(UA.conj().T), C, 0.0, None, f32), UB, 0.0, None, f32)
+    Y = solve_sylv_tri(TA, TB, Ct, f32)
+    X = gemm(1.0, gemm(1.0, UA, Y, 0.0, None, f32), np.ascontiguousarray(UB.conj().T), 0.0, None, f32)
+    return X, residual(A, B, C, X)

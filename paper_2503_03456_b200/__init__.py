@@ -21,7 +21,7 @@ from .precision import (B24, BFLOAT16, BINARY16, BINARY32, BINARY64, FORMATS, TF
                         PrecisionContext, format_from_name, parse_format)
 from .refinement import RefinementConfig, SolveReport, mp_inv, mp_orth, solve, solve_pert_sylv_tri_stat
 from .batch import gather_solutions, shard_range, solve_batched
-from .sylvester import SylvesterProblem, residual, solve_sylv_tri
+from .sylvester import DirectSolveReport, SylvesterProblem, bartels_stewart, residual, solve_sylv_tri
 from .linalg import QrFactors, SchurFactors, gemm, mgs_qr, schur
 
 __version__ = "0.1.0"

@@ -19,7 +19,7 @@ OK, SINGULAR_EQUATION, NUMERIC_BREAKDOWN, ITERATION_LIMIT = 0, 1, 2, 3
 RANK_DEFICIENT, SINGULAR_MATRIX, FORMAT_OVERFLOW, NON_CONVERGENCE = 4, 5, 6, 7
 EINVAL, EUNSUPPORTED, EWORKSPACE = -1, -2, -3
 KIND_GENERAL, KIND_LYAPUNOV = 0, 1
-VARIANT_ORTH, VARIANT_INV = 0, 1
+VARIANT_ORTH, VARIANT_INV, VARIANT_BS = 0, 1, 2
 STAGE_REFINEMENT, STAGE_INITIAL, STAGE_DIVERGED = 0, 1, 2
 MAX_NORMS = 256
 DTYPE = {"float32": 0, "float64": 1, "complex64": 2, "complex128": 3}

@@ -46,7 +46,10 @@ def flops(algorithm: str, m: int, n: int, k: int = 0) -> FlopCount:
 
 
 def algorithm_name(variant: str, kind: str) -> str:
-    return f"mp_{variant}_{'lyap' if kind == 'lyapunov' else 'sylv'}"
+    suffix = "lyap" if kind == "lyapunov" else "sylv"
+    if variant == "bs":
+        return f"bartels_stewart_{suffix}"
+    return f"mp_{variant}_{suffix}"
 
 
 def gemm_phase_flops(m: int, n: int, k: int, kind: str = "general") -> float:

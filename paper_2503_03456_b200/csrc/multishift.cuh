@@ -35,7 +35,7 @@ constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
 // rows/columns; the two phases order the only overlapping entries.  The warp
 // ops are branch-free (warp_left3 / warp_right3 redirect idle lanes to a dummy
 // row/column of the smem window).
-constexpr int KMAX = 4;  // bulge chains in flight per sweep (one CTA each)
+constexpr int KMAX = 8;  // bulge chains in flight per sweep (one CTA each)
 template <class S>
 struct ChaseJobs {
   int ws[KMAX], we[KMAX], t0[KMAX], t1[KMAX];

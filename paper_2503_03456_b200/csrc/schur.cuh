@@ -334,6 +334,8 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     }
     if (loc.sweeps >= limit) { loc.status = ST_ITERLIMIT; break; }
     static const int kmax_env = getenv("MSY_CHAINS") ? atoi(getenv("MSY_CHAINS")) : KMAX;
+    // bulges per chain (a chain of nb bulges spans 4 nb rows of the W-row chase window)
+    static const int NBc = std::max(2, std::min(MsCfg<S>::NB, getenv("MSY_NB") ? atoi(getenv("MSY_NB")) : MsCfg<S>::NB));
     bool exc = (stag > 0 && stag % 6 == 0);
     // ---- aggressive early deflation on the trailing window (aed.cuh) ----
     static const int aed_on = getenv("MSY_AED") ? atoi(getenv("MSY_AED")) : 0;
@@ -377,8 +379,8 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     int nb, K = 1, ns;
     if (aed_ls >= 8) {  // shifts: the undeflated window eigenvalues, bottom-most first
       const int npairs = aed_ls / 2 - 1;
-      nb = std::min({MsCfg<S>::NB, npairs, std::max(1, (sz - 8) / 8)});
-      if (nb == MsCfg<S>::NB && kmax_env > 1)
+      nb = std::min({NBc, npairs, std::max(1, (sz - 8) / 8)});
+      if (nb == NBc && kmax_env > 1)
         K = std::max(1, std::min({std::min(kmax_env, KMAX), npairs / nb, sz / (12 * nb)}));
       pair_shifts_kernel<S><<<1, 32, 0, st>>>(aed_ls, w.wr, w.wi, nb * K, w.shifts, 0, A, lda, lo, hi, w.dinfo + 24);
       MSY_LAUNCH_CK();
@@ -390,10 +392,10 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
       loc.ms_sweeps++;
       continue;
     }
-    nb = std::min(MsCfg<S>::NB, std::max(1, (sz - 8) / 8));
+    nb = std::min(NBc, std::max(1, (sz - 8) / 8));
     // several chains per sweep when the active block is large and the trailing
     // block that supplies their shifts fits the one-CTA kernel
-    if (nb == MsCfg<S>::NB && kmax_env > 1)
+    if (nb == NBc && kmax_env > 1)
       K = std::max(1, std::min({std::min(kmax_env, KMAX), EigCfg<S>::NMAX / (2 * nb), sz / (12 * nb)}));
     ns = 2 * nb * K;
     if (!exc) {

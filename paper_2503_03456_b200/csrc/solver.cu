@@ -259,6 +259,10 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
 }
 
 template <class Hh, class Ll>
+int final_report(int m, int n, const Hh* A, int lda, const Hh* B, int ldb, const Hh* C, int ldc, Hh* X, int ldx,
+                 SolveWs<Hh, Ll>& w, cudaStream_t st, sylv_report* rep);
+
+template <class Hh, class Ll>
 int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb, const Hh* C, int ldc, Hh* X, int ldx,
                void* wsp, size_t wsb, cudaStream_t st, sylv_report* rep) {
   const int m = p->m, n = p->n;
@@ -451,7 +455,25 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
   if (rc) return rc;
   tm.mark();  // 6
   // ---- 7. residual (sylvester.py:199-209) and backward error ----
-  rc = gemm<Hh>('N', 'N', m, n, m, Hh(1), A, lda, X, ldx, Hh(0), w.R, m, st);
+  rc = final_report<Hh, Ll>(m, n, A, lda, B, ldb, C, ldc, X, ldx, w, st, rep);
+  if (rc) return rc;
+  tm.mark();  // 7
+  MSY_CK(host_sync(st));
+  rep->ms_schur = tm.ms(0, 1);
+  rep->ms_orth = tm.ms(1, 2);
+  rep->ms_setup = tm.ms(2, 3);
+  rep->ms_y0 = tm.ms(3, 4);
+  rep->ms_refine = tm.ms(4, 5);
+  rep->ms_recover = tm.ms(5, 7);
+  rep->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return 0;
+}
+
+// residual (sylvester.py:199-209) and the north star's backward error, in fp64
+template <class Hh, class Ll>
+int final_report(int m, int n, const Hh* A, int lda, const Hh* B, int ldb, const Hh* C, int ldc, Hh* X, int ldx,
+                 SolveWs<Hh, Ll>& w, cudaStream_t st, sylv_report* rep) {
+  int rc = gemm<Hh>('N', 'N', m, n, m, Hh(1), A, lda, X, ldx, Hh(0), w.R, m, st);
   if (!rc) rc = gemm<Hh>('N', 'N', m, n, n, Hh(1), X, ldx, B, ldb, Hh(1), w.R, m, st);
   if (rc) return rc;
   double nr[3], nA[3], nB[3], nC[3], nX[3];
@@ -467,14 +489,81 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
   rep->residual = den == 0.0 ? 0.0 : num / den;
   rep->backward_error = (a + b) * x == 0.0 ? 0.0 : num / ((a + b) * x);
   rep->norm_x = x;
-  tm.mark();  // 7
+  return 0;
+}
+
+// Bartels-Stewart in one precision (sylvester.py:160-178, the paper's fp64 comparator):
+// Schur(A) || Schur(B) in Hh, F = U_A^H C U_B, Y = trsyl(T_A, T_B, F), X = U_A Y U_B^H.
+// A singular or non-finite triangular solve is reported as a typed failure at the
+// initial solve with X all NaN (the wrapper raises the reference's exceptions).
+template <class Hh>
+int bs_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb, const Hh* C, int ldc, Hh* X, int ldx,
+            void* wsp, size_t wsb, cudaStream_t st, sylv_report* rep) {
+  const int m = p->m, n = p->n;
+  Arena ar(wsp, wsb);
+  SolveWs<Hh, Hh> w;
+  SolveWs<Hh, Hh>::carve(ar, m, n, p->kind, SYLV_VARIANT_ORTH, w);
+  if (!ar.ok()) return SYLV_EWORKSPACE;
+  int rc = ctx_init();
+  if (rc) return rc;
+  memset(rep, 0, sizeof(*rep));
+  rep->fail_row = rep->fail_col = -1;
+  auto t0 = std::chrono::steady_clock::now();
+  HostTimer tm(st);
+  tm.mark();  // 0
+  const bool lyap = p->kind == SYLV_KIND_LYAPUNOV;
+  int* ovf = w.ints + 32;
+  MSY_CK(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
+  SchurStats sa{}, sb{};
+  rc = run_schur_pair<Hh, Hh>(m, n, p->kind, A, lda, B, ldb, w, st, ovf, &sa, &sb);
+  if (rc) return rc;
+  rep->schur_sweeps_a = sa.sweeps;
+  rep->schur_sweeps_b = sb.sweeps;
+  MSY_CK(host_sync(st));
+  if (sa.status || sb.status) { rep->status = SYLV_ITERATION_LIMIT; return 0; }
+  tm.mark();  // 1
+  rc = gemm<Hh>('C', 'N', m, n, m, Hh(1), w.UA, m, C, ldc, Hh(0), w.tmp, m, st);
+  if (!rc) rc = gemm<Hh>('N', 'N', m, n, n, Hh(1), w.tmp, m, w.UB, n, Hh(0), w.F, m, st);
+  if (rc) return rc;
+  tm.mark();  // 2
+  int* tstat = w.ints;
+  trsyl_status_init<<<1, 1, 0, st>>>(tstat);
+  MSY_LAUNCH_CK();
+  rc = trsyl<Hh>(m, n, w.TA, m, w.TB, n, lyap ? 1 : 0, w.F, m, w.tsh, tstat, st);
+  if (rc) return rc;
+  int row = -1, col = -1;
+  int ts = read_trsyl_status(tstat, m, n, lyap ? 1 : 0, &row, &col, st);
+  if (ts < 0) return ts;
+  if (ts == SYLV_OK) {
+    double o[3];
+    rc = read_reduce<Hh>(w.F, m, n, m, nullptr, 0, 0, w.part, w.red, o, st);
+    if (rc) return rc;
+    if (!std::isfinite(o[0])) ts = SYLV_NUMERIC_BREAKDOWN;
+  }
+  if (ts != SYLV_OK) {
+    rep->status = ts;
+    rep->fail_stage = SYLV_STAGE_INITIAL;
+    rep->fail_row = row;
+    rep->fail_col = col;
+    rep->residual = NAN;
+    fill<Hh>(m, n, mk<Hh>(NAN, NAN), X, ldx, st);
+    MSY_CK(host_sync(st));
+    return 0;
+  }
+  tm.mark();  // 3
+  rc = gemm<Hh>('N', 'N', m, n, m, Hh(1), w.UA, m, w.F, m, Hh(0), w.tmp, m, st);
+  if (!rc) rc = gemm<Hh>('N', 'C', m, n, n, Hh(1), w.tmp, m, w.UB, n, Hh(0), X, ldx, st);
+  if (rc) return rc;
+  tm.mark();  // 4
+  rc = final_report<Hh, Hh>(m, n, A, lda, B, ldb, C, ldc, X, ldx, w, st, rep);
+  if (rc) return rc;
+  rep->converged = 1;
+  tm.mark();  // 5
   MSY_CK(host_sync(st));
   rep->ms_schur = tm.ms(0, 1);
-  rep->ms_orth = tm.ms(1, 2);
-  rep->ms_setup = tm.ms(2, 3);
-  rep->ms_y0 = tm.ms(3, 4);
-  rep->ms_refine = tm.ms(4, 5);
-  rep->ms_recover = tm.ms(5, 7);
+  rep->ms_setup = tm.ms(1, 2);
+  rep->ms_y0 = tm.ms(2, 3);
+  rep->ms_recover = tm.ms(3, 5);
   rep->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return 0;
 }
@@ -540,8 +629,10 @@ static int check_params(const sylv_params* p) {
   if (!p || p->m < 1 || p->n < 1 || p->max_iter < 1) return SYLV_EINVAL;
   if (p->kind != SYLV_KIND_GENERAL && p->kind != SYLV_KIND_LYAPUNOV) return SYLV_EINVAL;
   if (p->kind == SYLV_KIND_LYAPUNOV && p->m != p->n) return SYLV_EINVAL;
-  if (p->variant != SYLV_VARIANT_ORTH && p->variant != SYLV_VARIANT_INV) return SYLV_EINVAL;
+  if (p->variant != SYLV_VARIANT_ORTH && p->variant != SYLV_VARIANT_INV && p->variant != SYLV_VARIANT_BS)
+    return SYLV_EINVAL;
   if (p->low_bits != 32 && p->low_bits != 64) return SYLV_EUNSUPPORTED;
+  if (p->variant == SYLV_VARIANT_BS && p->low_bits != 64) return SYLV_EUNSUPPORTED;
   if (p->correction_bits != 32 && p->correction_bits != 64) return SYLV_EUNSUPPORTED;
   return 0;
 }
@@ -567,6 +658,13 @@ int sylv_solve(const sylv_params* p, const void* A, int lda, const void* B, int 
   if (rc) return rc;
   if (!A || !B || !C || !X || !rep || lda < p->m || ldb < p->n || ldc < p->m || ldx < p->m) return SYLV_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  if (p->variant == SYLV_VARIANT_BS) {
+    if (!p->complex_data)
+      return bs_impl<double>(p, (const double*)A, lda, (const double*)B, ldb, (const double*)C, ldc, (double*)X,
+                             ldx, ws, ws_bytes, st, rep);
+    return bs_impl<cdouble>(p, (const cdouble*)A, lda, (const cdouble*)B, ldb, (const cdouble*)C, ldc,
+                            (cdouble*)X, ldx, ws, ws_bytes, st, rep);
+  }
   if (!p->complex_data) {
     if (p->low_bits == 32)
       return solve_impl<double, float>(p, (const double*)A, lda, (const double*)B, ldb, (const double*)C, ldc,

@@ -20,8 +20,10 @@
 
 namespace msy {
 
-template <class S> struct TrsylCfg { static constexpr int NB = 64; };
-template <> struct TrsylCfg<cdouble> { static constexpr int NB = 32; };
+// LEAF2: two-level leaf (sub-tile wavefront); measured faster for the 64-wide leaves,
+// slower for the 32-wide complex128 leaves, which keep the single-level wavefront
+template <class S> struct TrsylCfg { static constexpr int NB = 64; static constexpr bool LEAF2 = true; };
+template <> struct TrsylCfg<cdouble> { static constexpr int NB = 32; static constexpr bool LEAF2 = false; };
 
 enum { TRS_OK = 0, TRS_SINGULAR = 1, TRS_BREAKDOWN = 2 };
 
@@ -102,6 +104,7 @@ __device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int 
       for (int c2 = 0; c2 < QQ; c2++) M[u][r + PP * c2] = M[u][r + PP * c2] + Bs[(j + c2) + (j + c) * P];
     }
   bool ok = true;
+  S dinv[NS];  // reciprocal pivots: the back substitution multiplies (no divisions on the chain)
 #pragma unroll
   for (int c = 0; c < NS; c++) {
     // partial pivoting by swapping values (indices stay compile-time constants)
@@ -115,6 +118,7 @@ __device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int 
     }
     if (abs1(M[c][c]) == R(0)) ok = false;
     const S inv = ok ? S(1) / M[c][c] : S(0);
+    dinv[c] = inv;
 #pragma unroll
     for (int r = c + 1; r < NS; r++) {
       const S f = M[r][c] * inv;
@@ -128,7 +132,7 @@ __device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int 
     S s = x[c];
 #pragma unroll
     for (int v = c + 1; v < NS; v++) s = s - M[c][v] * x[v];
-    x[c] = s / M[c][c];
+    x[c] = s * dinv[c];
   }
 #pragma unroll
   for (int c = 0; c < QQ; c++)
@@ -179,10 +183,7 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
   S* As = (S*)smem_raw;      // [k][i], ld P   (K up to NB+1)
   S* Bs = As + P * P;        // [k][j], ld P
   S* Ws = Bs + P * P;        // W block, [i + j*P]
-  __shared__ int ru_rank[NB + 2], cu_rank[NB + 2];
-  __shared__ int ru_of[NB + 2], cu_of[NB + 2];  // rank -> first row / column of the unit
-  __shared__ int nru, ncu;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int tr_ = tid % TG, tc = tid / TG;
   S acc[RM][RM];
 #pragma unroll
@@ -262,6 +263,184 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
     }
   }
   if (!solve) return;
+  if constexpr (TrsylCfg<S>::LEAF2) {
+  // ---- leaf: TA_II Y + Y TB_JJ = W_IJ in shared memory ----
+  // Two levels: the leaf is cut into sub-tiles of ~LST x LST (edges nudged so no 2x2
+  // block is split); sub-tile anti-diagonals are processed in order.  On each, one
+  // warp per sub-tile solves it with an element-level wavefront over its 1x1 / 2x2
+  // units (warp-synchronous), then every pending sub-tile takes the contributions of
+  // the sub-tiles just solved (small shared-memory GEMMs, one warp per sub-tile).
+  for (int e = tid; e < bi * bi; e += nt) {
+    int i = e % bi, k = e / bi;
+    As[i + k * P] = TA[(i0 + i) + (size_t)(i0 + k) * lda];
+  }
+  for (int e = tid; e < bj * bj; e += nt) {
+    int i = e % bj, k = e / bj;
+    Bs[i + k * P] = TB[(j0 + i) + (size_t)(j0 + k) * ldb];
+  }
+  __syncthreads();
+  constexpr int LST = 8, LSM = LST + 1, NSUB = (NB + 1 + LST - 1) / LST + 1;
+  constexpr int NWARP = TRS_TPB / 32;
+  __shared__ int sr[NSUB + 1], sc[NSUB + 1], s_nsr, s_nsc;
+  if (tid == 0) {  // sub-tile edges: rows in index order, columns in solve order
+    int c = 0, b0 = 0;
+    while (b0 < bi) {
+      int e1 = min(b0 + LST, bi);
+      if (e1 < bi && !iszero(As[e1 + (e1 - 1) * P])) e1++;
+      sr[c++] = b0;
+      b0 = e1;
+    }
+    sr[c] = bi;
+    s_nsr = c;
+    c = 0; b0 = 0;
+    while (b0 < bj) {
+      int e1 = min(b0 + LST, bj);
+      if (e1 < bj && !iszero(lowerB ? Bs[(e1 - 1) + e1 * P] : Bs[e1 + (e1 - 1) * P])) e1++;
+      sc[c++] = b0;
+      b0 = e1;
+    }
+    sc[c] = bj;
+    s_nsc = c;
+  }
+  __syncthreads();
+  const int nsr = s_nsr, nsc = s_nsc;
+  // sub-tile of row rank a (from the bottom) / column rank b (solve order)
+  auto rows_of = [&](int a, int& r0, int& r1) { const int I = nsr - 1 - a; r0 = sr[I]; r1 = sr[I + 1]; };
+  auto cols_of = [&](int bb, int& c0, int& c1) { const int J = lowerB ? nsc - 1 - bb : bb; c0 = sc[J]; c1 = sc[J + 1]; };
+  __shared__ int u_of[NWARP][2][LSM + 1], u_len[NWARP][2][LSM + 1], u_rank[NWARP][2][LSM + 1], u_n[NWARP][2];
+  for (int s = 0; s < nsr + nsc - 1; s++) {
+    // ---- solve the sub-tiles on anti-diagonal s (one warp each) ----
+    const int alo = max(0, s - (nsc - 1)), ahi = min(s, nsr - 1);
+    for (int a = alo + warp; a <= ahi; a += NWARP) {
+      const int bb = s - a;
+      int r0, r1, c0, c1;
+      rows_of(a, r0, r1);
+      cols_of(bb, c0, c1);
+      const int ri = r1 - r0, cj = c1 - c0;
+      int* rof = u_of[warp][0]; int* rln = u_len[warp][0]; int* rrk = u_rank[warp][0];
+      int* cof = u_of[warp][1]; int* cln = u_len[warp][1]; int* crk = u_rank[warp][1];
+      if (lane == 0) {
+        int cnt = 0, i = r1 - 1;  // row units from the bottom
+        while (i >= r0) {
+          const int st2 = (i > r0 && !iszero(As[i + (i - 1) * P])) ? i - 1 : i;
+          for (int q = st2; q <= i; q++) rrk[q - r0] = cnt;
+          rof[cnt] = st2; rln[cnt] = i - st2 + 1; cnt++;
+          i = st2 - 1;
+        }
+        u_n[warp][0] = cnt;
+        cnt = 0;
+        if (!lowerB) {
+          int j = c0;
+          while (j < c1) {
+            const int len = (j + 1 < c1 && !iszero(Bs[(j + 1) + j * P])) ? 2 : 1;
+            for (int q = j; q < j + len; q++) crk[q - c0] = cnt;
+            cof[cnt] = j; cln[cnt] = len; cnt++;
+            j += len;
+          }
+        } else {
+          int j = c1 - 1;
+          while (j >= c0) {
+            const int st2 = (j > c0 && !iszero(Bs[(j - 1) + j * P])) ? j - 1 : j;
+            for (int q = st2; q <= j; q++) crk[q - c0] = cnt;
+            cof[cnt] = st2; cln[cnt] = j - st2 + 1; cnt++;
+            j = st2 - 1;
+          }
+        }
+        u_n[warp][1] = cnt;
+      }
+      __syncwarp();
+      const int nru = u_n[warp][0], ncu = u_n[warp][1];
+      constexpr int EPL = (LSM * LSM + 31) / 32;
+      int ei[EPL], ej[EPL], era[EPL], ecr[EPL];
+#pragma unroll
+      for (int k = 0; k < EPL; k++) {
+        const int e = lane + 32 * k;
+        if (e < ri * cj) {
+          ei[k] = r0 + e % ri; ej[k] = c0 + e / ri;
+          era[k] = rrk[ei[k] - r0]; ecr[k] = crk[ej[k] - c0];
+        } else {
+          ei[k] = 0; ej[k] = 0; era[k] = -1000000; ecr[k] = -1000000;
+        }
+      }
+      for (int t = 0; t < nru + ncu - 1; t++) {
+        if (lane < nru) {  // lane a solves unit (a, t - a)
+          const int ua = lane, ub = t - lane;
+          if (ub >= 0 && ub < ncu) {
+            const int i = rof[ua], p = rln[ua], jst = cof[ub], q = cln[ub];
+            bool ok = true;
+            if (p == 1 && q == 1) {
+              const S dd = As[i + i * P] + Bs[jst + jst * P];
+              ok = !iszero(dd);
+              Ws[i + jst * P] = ok ? Ws[i + jst * P] / dd : mk<S>(NAN, NAN);
+            } else if (p == 2 && q == 1) {
+              ok = unit_solve<S, 2, 1>(As, Bs, Ws, P, i, jst);
+            } else if (p == 1 && q == 2) {
+              ok = unit_solve<S, 1, 2>(As, Bs, Ws, P, i, jst);
+            } else {
+              ok = unit_solve<S, 2, 2>(As, Bs, Ws, P, i, jst);
+            }
+            if (!ok) {  // singular diagonal pair: report the first in reference order (decoded on the host)
+              const int jg = j0 + jst, ig = i0 + i + p - 1;
+              const int crank = lowerB ? (n - 1 - jg) : jg;
+              atomicMin(&status[0], crank * m + (m - 1 - ig));
+            }
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < EPL; k++) {
+          const int ra = era[k], cr = ecr[k];
+          if (ra + cr > t) {
+            const int i = ei[k], j = ej[k];
+            S v = Ws[i + j * P];
+            const int rs = t - cr;
+            if (rs >= 0 && rs < ra) {
+              const int st2 = rof[rs];
+              v = v - As[i + st2 * P] * Ws[st2 + j * P];
+              if (rln[rs] == 2) v = v - As[i + (st2 + 1) * P] * Ws[(st2 + 1) + j * P];
+            }
+            const int cs = t - ra;
+            if (cs >= 0 && cs < cr) {
+              const int st2 = cof[cs];
+              v = v - Ws[i + st2 * P] * Bs[st2 + j * P];
+              if (cln[cs] == 2) v = v - Ws[i + (st2 + 1) * P] * Bs[(st2 + 1) + j * P];
+            }
+            Ws[i + j * P] = v;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // ---- pending sub-tiles take the contributions of diagonal s ----
+    for (int it = warp; it < nsr * nsc; it += NWARP) {
+      const int a = it % nsr, bb = it / nsr;
+      if (a + bb <= s) continue;
+      const int as = s - bb, bs = s - a;  // solved tile in my column (below) / in my row (before)
+      const bool pa = as >= 0 && as < a, pb = bs >= 0 && bs < bb;
+      if (!pa && !pb) continue;
+      int r0, r1, c0, c1;
+      rows_of(a, r0, r1);
+      cols_of(bb, c0, c1);
+      const int ri = r1 - r0, cj = c1 - c0;
+      int k0 = 0, k1 = 0, l0 = 0, l1 = 0;
+      if (pa) rows_of(as, k0, k1);
+      if (pb) cols_of(bs, l0, l1);
+      for (int e = lane; e < ri * cj; e += 32) {
+        const int i = r0 + e % ri, j = c0 + e / ri;
+        S v = Ws[i + j * P];
+        for (int k = k0; k < k1; k++) v = v - As[i + k * P] * Ws[k + j * P];
+        for (int l = l0; l < l1; l++) v = v - Ws[i + l * P] * Bs[l + j * P];
+        Ws[i + j * P] = v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < bi * bj; e += nt) {
+    int i = e % bi, j = e / bi;
+    W[(i0 + i) + (size_t)(j0 + j) * ldw] = Ws[i + j * P];
+  }
+  } else {
   // ---- leaf: TA_II Y + Y TB_JJ = W_IJ in shared memory ----
   // element-level anti-diagonal wavefront over 1x1 / 2x2 units: sub-step s solves the
   // units (a, b) with a + b = s (a = row-unit rank from the bottom, b = column-unit
@@ -277,6 +456,9 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
     Bs[i + k * P] = TB[(j0 + i) + (size_t)(j0 + k) * ldb];
   }
   __syncthreads();
+  __shared__ int ru_rank[NB + 2], cu_rank[NB + 2];
+  __shared__ int ru_of[NB + 2], cu_of[NB + 2];  // rank -> first row / column of the unit
+  __shared__ int nru, ncu;
   __shared__ int ru_len[NB + 2], cu_len[NB + 2];
   if (tid == 0) {
     // row units from the bottom (rank 0 = bottom unit); 2x2 if As[i][i-1] != 0
@@ -382,6 +564,7 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
   for (int e = tid; e < bi * bj; e += nt) {
     int i = e % bi, j = e / bi;
     W[(i0 + i) + (size_t)(j0 + j) * ldw] = Ws[i + j * P];
+  }
   }
 }
 

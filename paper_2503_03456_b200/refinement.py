@@ -132,7 +132,8 @@ def solve(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, *, kind: str = "gen
     """Torch-native entry: A (m x m), B (n x n), C (m x n) row-major device tensors.
 
     float64 tensors take the real path (fp32 Schur), complex128 the complex
-    path (complex64 Schur).  Returns (X, native report).  Raises the
+    path (complex64 Schur).  variant: "orth" (mp_orth), "inv" (mp_inv) or "bs"
+    (the fp64 Bartels-Stewart comparator: Schur in binary64, no refinement).  Returns (X, native report).  Raises the
     reference's exception types for raised errors; typed failures are in
     ``report.status`` (see ``_failure_string``).
     """
@@ -149,6 +150,8 @@ def solve(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, *, kind: str = "gen
     if out is None:
         out = torch.empty((m, n), dtype=dt, device=A.device)
     # column-major problem (A' = B^T, B' = A^T, C' = C^T) of order (n, m)
+    if variant == "bs":
+        low_bits = 64
     rep = _solve_cm(B, A, C, out, n, m, kind, variant, low_bits, correction_bits,
                     epsilon if epsilon is not None else 1e-12 * max(m, n), max_iter, y0_zero)
     return out, rep
@@ -160,7 +163,7 @@ def _solve_cm(A, B, C, X, m, n, kind, variant, low_bits, correction_bits, epsilo
     p.m, p.n = m, n
     p.kind = _native.KIND_LYAPUNOV if kind == "lyapunov" else _native.KIND_GENERAL
     p.complex_data = int(A.is_complex())
-    p.variant = _native.VARIANT_INV if variant == "inv" else _native.VARIANT_ORTH
+    p.variant = {"inv": _native.VARIANT_INV, "bs": _native.VARIANT_BS}.get(variant, _native.VARIANT_ORTH)
     p.low_bits = int(low_bits)
     p.correction_bits = int(correction_bits)
     p.max_iter = int(max_iter)

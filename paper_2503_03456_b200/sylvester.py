@@ -1,9 +1,10 @@
 """``SylvesterProblem``, ``residual`` and the triangular solver entry point.
 
 Mirrors pkg/src/mpsylv/sylvester.py:47-90 (SylvesterProblem, same validation
-and kinds), :111-157 (solve_sylv_tri, device-backed by ``sylv_trsyl``) and
-:199-209 (residual, the binary64 relative residual, here evaluated on the
-device).
+and kinds), :111-157 (solve_sylv_tri, device-backed by ``sylv_trsyl``),
+:160-178 (bartels_stewart, the fp64 comparator, device-backed by ``sylv_solve``
+with SYLV_VARIANT_BS) and :199-209 (residual, the binary64 relative residual,
+here evaluated on the device).
 """
 
 from __future__ import annotations
@@ -135,3 +136,52 @@ def solve_sylv_tri(T_A, T_B, C, ctx=None, dev=None) -> np.ndarray:
     if info[0] == _native.NUMERIC_BREAKDOWN:
         raise NumericBreakdownError("non-finite values in the triangular solve")
     return D.from_cm(tW).astype(np.complex128)
+
+
+@dataclass
+class DirectSolveReport:
+    """Mirror of the reference's DirectSolveReport (sylvester.py:93-97).  The device path
+    does not return the Schur factors (schur_A / schur_B are None); backward_error and
+    timings are extra fields."""
+
+    residual: float
+    schur_A: object = None
+    schur_B: object = None
+    backward_error: float = float("nan")
+    timings: dict | None = None
+
+
+def bartels_stewart(p, ctx=None, dev=None):
+    """Schur-transform, solve the triangular equation, transform back (sylvester.py:160-178).
+
+    All in binary64 (the reference's default context and the paper's comparator);
+    kind='lyapunov' computes one Schur factorisation.  Returns (X, DirectSolveReport).
+    Raises SingularEquationError / NumericBreakdownError from the triangular solve and
+    IterationLimitError from the Schur factorisation, like the reference.
+    """
+    from .precision import format_bits
+    from .errors import IterationLimitError, UnsupportedPrecisionError
+    from .refinement import _solve_cm
+    if ctx is not None and format_bits(ctx.format) != 64:
+        raise UnsupportedPrecisionError("the device Bartels-Stewart path runs in binary64")
+    if not isinstance(p, SylvesterProblem):
+        p = SylvesterProblem(p.A, p.B, p.C, kind=getattr(p, "kind", "general"))
+    m, n = p.m, p.n
+    dev = D.device(dev)
+    real = _is_real(p.A, p.B, p.C)
+    dt = torch.float64 if real else torch.complex128
+    cv = (lambda M: D.to_cm(np.real(M) if real else M, dt, dev))
+    tA, tB, tC = cv(p.A), cv(p.B), cv(p.C)
+    tX = torch.empty_like(tC)
+    rep = _solve_cm(tA, tB, tC, tX, m, n, "lyapunov" if p.kind == "lyapunov" else "general", "bs", 64, 64,
+                    0.0, 1, False)
+    if rep.status == _native.ITERATION_LIMIT:
+        raise IterationLimitError("QR iteration did not converge within its sweep budget")
+    if rep.status == _native.SINGULAR_EQUATION:
+        raise SingularEquationError(rep.fail_row, rep.fail_col)
+    if rep.status == _native.NUMERIC_BREAKDOWN:
+        raise NumericBreakdownError("non-finite values in the triangular solve")
+    X = D.from_cm(tX).astype(np.complex128)
+    return X, DirectSolveReport(float(rep.residual), None, None, float(rep.backward_error),
+                                dict(schur=rep.ms_schur, transform=rep.ms_setup, trsyl=rep.ms_y0,
+                                     recover=rep.ms_recover, total=rep.ms_total))

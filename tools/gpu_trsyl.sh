@@ -1,0 +1,5 @@
+for t in f32 f64; do timeout 300 python tools/trsyl_only.py 4096 $t 3; done
+timeout 300 python tools/trsyl_only.py 1000 f64 2
+timeout 300 python tools/trsyl_only.py 130 f64 2
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 600 python tools/probe.py big 2>&1 | grep -v "^schur"
