@@ -192,6 +192,28 @@ def ktimer(L, op):
     return [(cnt[i], ms[i], fl[i]) for i in range(n)]
 
 
+KPREFIX = {0: "gemm_dmma", 1: "gemm_simt", 2: "apply_z", 3: "chase", 4: "trsyl", 5: "hess", 6: "schur", 7: "aed"}
+
+
+def ncu_traffic(cls):
+    """Per-launch DRAM bytes of a kernel class from the newest committed `ncu --set full` capture
+    (profiles/*ncu_full_capture.json), or (None, None)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full_capture.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            with open(f) as fh:
+                cap = json.load(fh)
+        except Exception:
+            continue
+        ls = [l for l in cap.get("launches", []) if l.get("kernel", "").startswith(KPREFIX.get(cls, "?"))]
+        if ls:
+            return (sum(l["dram_bytes"] for l in ls) / len(ls),
+                    f"{os.path.relpath(f, ROOT)}: mean over {len(ls)} captured launches (grids "
+                    f"{sorted({l['grid'] for l in ls})})")
+    return None, None
+
+
 def kernel_rooflines(rows, pk, steps):
     """Per kernel class: launches, event-timed ms per step, share of the summed kernel time, achieved
     TFLOP/s from the algorithmic flops declared at each launch.  roofline = the dominant class that
@@ -217,8 +239,10 @@ def kernel_rooflines(rows, pk, steps):
         c, ms, fl = rows[best]
         ach = fl / (ms * 1e-3) / 1e12
         peak = pk.get(KPEAK.get(best))
+        traffic, tsrc = ncu_traffic(best)
         roof = {"bound": "tensor" if best == 0 else "fp32-simt", "kernel": KCLASSES[best], "achieved": ach,
-                "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if peak else None, "traffic": None,
+                "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if peak else None, "traffic": traffic,
+                "traffic_source": tsrc,
                 "share_of_kernel_time": ms / tot,
                 "peak_source": ("measured live by sylv_microbench (DMMA.8x8x4 / FFMA loops); MEASURED_PEAKS.json "
                                 "has no fp32/fp64 figure"),
@@ -474,6 +498,13 @@ def run_c4(args):
             evs[i][1].record(st)
         torch.cuda.synchronize(dev)
     launches = (L.sylv_launch_count() - launches0) // max(1, args.steps)
+    ktimer(L, 1)  # per-kernel-class event timing over a repetition of the timed steps
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        step()
+    torch.cuda.synchronize(dev)
+    krows = ktimer(L, 2)
+    ktimer(L, 0)
     total_ms = sum(a.elapsed_time(b) for a, b in evs)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -508,9 +539,10 @@ def run_c4(args):
         es = hA.element_size()
         e2e = {"value": max(1, args.steps) * total / (tot / 1e3), "unit": "solves/s",
                "h2d_bytes_per_step": cnt * 3 * m * m * es, "d2h_bytes_per_step": cnt * m * m * es}
-    roof = sol_roof = cpu = None
+    roof = sol_roof = cpu = kern = gemm_roof = None
     if rank == 0:
-        roof, pk = dmma_roofline(L, st, dev, m)
+        gemm_roof, pk = dmma_roofline(L, st, dev, m)
+        roof, kern = kernel_rooflines(krows, pk, args.steps)
         sol_roof = solve_roofline(pk, "orth", "general", m, m, max(ks), False, total_ms / args.steps / 1e3,
                                   cnt)
         if world == 1 and not args.no_cpu_baseline:
@@ -531,7 +563,8 @@ def run_c4(args):
                                                         "total")},
                        "l2": "flushed between steps (256 MiB write); per-rank working set >> 126 MB L2",
                        "parallelism": f"shard x{world} + gather"},
-            "roofline": roof, "solve_roofline": sol_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "gemm_phase_roofline": gemm_roof, "kernels": kern, "solve_roofline": sol_roof,
+            "cpu_baseline": cpu, "e2e": e2e,
             "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
             "gpu_launches": int(launches),
             "measured_peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},

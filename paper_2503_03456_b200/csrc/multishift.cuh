@@ -14,6 +14,8 @@
 //   * shifts: eigenvalues of the trailing ns x ns block (schur_small_kernel in
 //     eigenvalue mode), exceptional shifts after 6 stagnant sweeps.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "schur_small.cuh"
 
@@ -243,6 +245,100 @@ __global__ void __launch_bounds__(256) apply_z_multi_kernel(S* H, int ldh, S* U,
   while (j + 1 < jobs.n && (int)blockIdx.x >= jobs.start[j + 1]) j++;
   apply_z_block<S>(blockIdx.x - jobs.start[j], smem_raw, jobs.nz[j], jobs.Z[j], H, ldh, jobs.r0[j], jobs.cL0[j],
                    jobs.cL1[j], jobs.rlo[j], jobs.rR1[j], U, ldu, jobs.mU[j]);
+}
+
+// ---------------------------------------------------------------------------
+// Z application split over a thread-block cluster: the 32-column (region L) or 32-row
+// (regions R, U) tile of a job is shared by the AZC CTAs of one cluster, each producing
+// 32 of the nz output rows (L) / columns (R, U) from its 32-wide slice of Z.  Every CTA
+// stages the whole nz-deep input tile before the cluster barrier, so the in-place writes
+// that follow cannot race with a sibling's reads.  Five times the CTAs of apply_z_multi
+// for the same region, each with a 40 KB footprint (several CTAs per SM): the near-window
+// applications on the sweep's critical path finish in a fraction of the time.
+template <class S> struct Azc { static constexpr int N = (MsCfg<S>::W + 31) / 32; };  // CTAs per cluster
+constexpr int AZC_THREADS = 128, AZC_TP = 33, AZC_CP = 36;
+template <class S>
+static size_t azc_smem() { return (size_t)MsCfg<S>::W * (AZC_TP + AZC_CP) * sizeof(S); }
+template <class S>
+__global__ void __cluster_dims__(Azc<S>::N, 1, 1) __launch_bounds__(AZC_THREADS)
+    apply_z_cl_kernel(S* H, int ldh, S* U, int ldu, const ApplyJobs<S> jobs) {
+  constexpr int TP = AZC_TP, CP = AZC_CP;  // smem strides: input tile [k][32] (TP), Z slice [k][32] (CP)
+  constexpr int AZC = Azc<S>::N;
+  extern __shared__ __align__(16) unsigned char azc_raw[];
+  S* Ts = (S*)azc_raw;
+  S* Zc = Ts + MsCfg<S>::W * TP;
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int part = (int)cl.block_rank();
+  int b = blockIdx.x / AZC;
+  int j = 0;
+  while (j + 1 < jobs.n && b >= jobs.start[j + 1]) j++;
+  b -= jobs.start[j];
+  const int nz = jobs.nz[j], r0 = jobs.r0[j];
+  const S* __restrict__ Zg = jobs.Z[j];
+  const int cL0 = jobs.cL0[j], cL1 = jobs.cL1[j], rlo = jobs.rlo[j], rR1 = jobs.rR1[j], mU = jobs.mU[j];
+  const int ntL = cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0, ntR = rR1 > rlo ? cdiv(rR1 - rlo, 32) : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int o0 = part * 32;                 // this CTA's output slice
+  const int no = min(32, nz - o0);          // <= 0: nothing to write (still joins the barrier)
+  // slice of Z: columns o0..o0+no-1 (L uses conj(Z[k, o]), R/U use Z[k, o])
+  for (int e = tid; e < nz * 32; e += AZC_THREADS) {
+    const int k = e % nz, o = e / nz;
+    Zc[k * CP + o] = o < no ? Zg[k + (size_t)(o0 + o) * nz] : S(0);
+  }
+  if (b < ntL) {  // ---- region L: H[r0 + o, c] <- sum_k conj(Z[k, o]) H[r0 + k, c] ----
+    const int c0 = cL0 + b * 32, nc = min(32, cL1 - c0);
+    for (int e = tid; e < nz * 32; e += AZC_THREADS) {
+      const int k = e % nz, c = e / nz;
+      Ts[k * TP + c] = c < nc ? H[(r0 + k) + (size_t)(c0 + c) * ldh] : S(0);
+    }
+    cl.sync();
+    if (no > 0) {
+      S acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) acc[q] = S(0);
+      for (int k = 0; k < nz; k++) {
+        const S t = Ts[k * TP + lane];
+        const S* zr = Zc + k * CP + warp * 8;
+#pragma unroll
+        for (int q = 0; q < 8; q++) acc[q] = fmacc(zr[q], t, acc[q]);
+      }
+      if (lane < nc)
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const int o = warp * 8 + q;
+          if (o < no) H[(r0 + o0 + o) + (size_t)(c0 + lane) * ldh] = acc[q];
+        }
+    }
+    return;
+  }
+  b -= ntL;
+  S* M;
+  int ldm, rbase, nrows;
+  if (b < ntR) { M = H; ldm = ldh; rbase = rlo + b * 32; nrows = min(32, rR1 - rbase); }
+  else { b -= ntR; M = U; ldm = ldu; rbase = b * 32; nrows = min(32, mU - rbase); }
+  // ---- regions R / U: M[r, r0 + o] <- sum_k M[r, r0 + k] Z[k, o] ----
+  for (int e = tid; e < nz * 32; e += AZC_THREADS) {
+    const int r = e % 32, k = e / 32;
+    Ts[k * TP + r] = r < nrows ? M[(rbase + r) + (size_t)(r0 + k) * ldm] : S(0);
+  }
+  cl.sync();
+  if (no <= 0) return;
+  S acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; q++) acc[q] = S(0);
+  for (int k = 0; k < nz; k++) {
+    const S t = Ts[k * TP + lane];
+    const S* zr = Zc + k * CP + warp * 8;
+#pragma unroll
+    for (int q = 0; q < 8; q++) acc[q] = fmac(t, zr[q], acc[q]);
+  }
+  if (lane < nrows)
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int o = warp * 8 + q;
+      if (o < no) M[(rbase + lane) + (size_t)(r0 + o0 + o) * ldm] = acc[q];
+    }
 }
 
 template <class S>

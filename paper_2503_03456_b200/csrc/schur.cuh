@@ -109,6 +109,8 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
   MSY_SMEM_ATTR_ONCE(chase_kernel<S>, smem_max);
   MSY_SMEM_ATTR_ONCE(apply_z_kernel<S>, (int)applyz_smem<S>(W));
   MSY_SMEM_ATTR_ONCE(apply_z_multi_kernel<S>, (int)applyz_smem<S>(W));
+  MSY_SMEM_ATTR_ONCE(apply_z_cl_kernel<S>, (int)azc_smem<S>());
+  static const int azc_mode = getenv("MSY_AZC") ? atoi(getenv("MSY_AZC")) : 1;
   if (K < 1 || K > KMAX) return -5;
   const int span = hi - lo;
   const long Tn = 4L * (nb - 1) + span;
@@ -209,14 +211,17 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
           MSY_CK(cudaEventRecord(sc->evN, st));
           MSY_CK(cudaStreamWaitEvent(fst, sc->evN, 0));
         }
-        if (jr[f].start[nj] > 0) {
-          KScope ks(KC_APPLYZ, applyz_flops<S>(jr[f]), s2);
-          apply_z_multi_kernel<S><<<jr[f].start[nj], 256, applyz_smem<S>(W), s2>>>(H, ldh, U, ldu, jr[f]);
-          MSY_LAUNCH_CK();
-        }
-        if (jc[f].start[nj] > 0) {
-          KScope ks(KC_APPLYZ, applyz_flops<S>(jc[f]), s2);
-          apply_z_multi_kernel<S><<<jc[f].start[nj], 256, applyz_smem<S>(W), s2>>>(H, ldh, U, ldu, jc[f]);
+        // cluster-split application (apply_z_cl_kernel) for the near parts on the chase's
+        // critical path (MSY_AZC: 0 off, 1 near only, 2 near and far)
+        const bool cl = azc_mode >= 2 || (azc_mode == 1 && f == 0);
+        for (int rc_ = 0; rc_ < 2; rc_++) {
+          const ApplyJobs<S>& jb = rc_ == 0 ? jr[f] : jc[f];
+          if (jb.start[nj] <= 0) continue;
+          KScope ks(KC_APPLYZ, applyz_flops<S>(jb), s2);
+          if (cl)
+            apply_z_cl_kernel<S><<<jb.start[nj] * Azc<S>::N, AZC_THREADS, azc_smem<S>(), s2>>>(H, ldh, U, ldu, jb);
+          else
+            apply_z_multi_kernel<S><<<jb.start[nj], 256, applyz_smem<S>(W), s2>>>(H, ldh, U, ldu, jb);
           MSY_LAUNCH_CK();
         }
       }

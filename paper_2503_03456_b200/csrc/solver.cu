@@ -76,6 +76,9 @@ struct SolveWs {
   double* part;
   double* red;
   int* ints;
+  Hh *GB, *tmpB;     // B-side scratch: orth(B) and S_B run beside the A side (mp_orth, Sylvester)
+  double *partB, *redB;
+  int* intsB;
   static void carve(Arena& ar, int m, int n, int kind, int variant, SolveWs& w) {
     size_t mm = (size_t)m * m, nn = (size_t)n * n, mn = (size_t)m * n;
     w.TA = ar.get<Ll>(mm);
@@ -106,6 +109,16 @@ struct SolveWs {
     w.part = ar.get<double>(3 * RED_BLOCKS);
     w.red = ar.get<double>(16);
     w.ints = ar.get<int>(64);
+    w.GB = w.tmpB = nullptr;
+    w.partB = w.redB = nullptr;
+    w.intsB = nullptr;
+    if (variant == SYLV_VARIANT_ORTH && kind != SYLV_KIND_LYAPUNOV) {
+      w.GB = ar.get<Hh>(nn);
+      w.tmpB = ar.get<Hh>(nn);
+      w.partB = ar.get<double>(3 * RED_BLOCKS);
+      w.redB = ar.get<double>(16);
+      w.intsB = ar.get<int>(16);
+    }
   }
 };
 
@@ -215,7 +228,8 @@ int refine_loop(int m, int n, const Hh* TAh, const Hh* TBh, int lowerB, const Hh
 
 template <class Hh, class Ll>
 int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, int ldb, SolveWs<Hh, Ll>& w,
-                   cudaStream_t st, int* ovf, SchurStats* sa, SchurStats* sb) {
+                   cudaStream_t st, int* ovf, SchurStats* sa, SchurStats* sb,
+                   const std::function<int(cudaStream_t)>* post_b = nullptr) {
   int rc = convert<Ll, Hh>(m, m, A, lda, w.TA, m, ovf, st);
   if (rc) return rc;
   SweepCtx* sca = t_serial_lane ? &g_ctx.serial : &g_ctx.swA;
@@ -248,6 +262,7 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
     host_sync_blocking() = blocking;
     rcb = convert<Ll, Hh>(n, n, B, ldb, w.TB, n, ovf_b, side);
     if (!rcb) rcb = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, side, sb, scb);
+    if (!rcb && post_b && sb->status == 0) rcb = (*post_b)(side);
   });
   rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, st, sa, &g_ctx.swA);
   tb.join();
@@ -283,7 +298,32 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
   MSY_CK(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
   // ---- 1. low-precision Schur pair ----
   SchurStats sa{}, sb{};
-  rc = run_schur_pair<Hh, Ll>(m, n, p->kind, A, lda, B, ldb, w, st, ovf, &sa, &sb);
+  // mp_orth, Sylvester: orth(B) and S_B = Q_B^H B Q_B run in the Schur(B) thread on its stream,
+  // overlapping the A side (the two chains are latency-bound small-kernel sequences)
+  const bool b_beside = !inv && !lyap && !t_serial_lane && w.GB != nullptr;
+  int b_rank = 0;
+  std::function<int(cudaStream_t)> post_b = [&](cudaStream_t ss) -> int {
+    int r2 = convert<Hh, Ll>(n, n, w.UB, n, w.TBh, n, nullptr, ss);
+    if (r2) return r2;
+    int* dflag = w.intsB;
+    double* ddiag = w.redB + 8;
+    MSY_CK(cudaMemsetAsync(dflag, 0, sizeof(int), ss));
+    fill<double>(1, 1, INFINITY, ddiag, 1, ss);
+    r2 = orth_cholqr<Hh>(n, w.TBh, n, w.QB, n, w.GB, n, dflag, ddiag, ss);
+    if (r2) return r2;
+    double o[3];
+    r2 = read_reduce<Hh>(w.TBh, n, n, n, nullptr, 0, 0, w.partB, w.redB, o, ss);
+    if (r2) return r2;
+    int hflag;
+    double hdiag;
+    MSY_CK(d2h(&hflag, dflag, sizeof(int), ss));
+    MSY_CK(d2h(&hdiag, ddiag, sizeof(double), ss));
+    if (hflag || hdiag <= n * tr<Hh>::u() * std::sqrt(o[0])) { b_rank = 1; return 0; }
+    r2 = gemm<Hh>('C', 'N', n, n, n, Hh(1), w.QB, n, B, ldb, Hh(0), w.tmpB, n, ss);
+    if (!r2) r2 = gemm<Hh>('N', 'N', n, n, n, Hh(1), w.tmpB, n, w.QB, n, Hh(0), w.SB, n, ss);
+    return r2;
+  };
+  rc = run_schur_pair<Hh, Ll>(m, n, p->kind, A, lda, B, ldb, w, st, ovf, &sa, &sb, b_beside ? &post_b : nullptr);
   if (rc) return rc;
   rep->schur_sweeps_a = sa.sweeps;
   rep->schur_sweeps_b = sb.sweeps;
@@ -315,6 +355,8 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
     if (hflag || hdiag <= m * tr<Hh>::u() * std::sqrt(o[0])) { rep->status = SYLV_RANK_DEFICIENT; return 0; }
     if (lyap) {
       rc = copy2d<Hh>(m, m, w.QA, m, w.QB, n, st);
+    } else if (b_beside) {
+      if (b_rank) { rep->status = SYLV_RANK_DEFICIENT; return 0; }
     } else {
       rc = convert<Hh, Ll>(n, n, w.UB, n, w.TBh, n, nullptr, st);
       if (rc) return rc;
@@ -341,7 +383,7 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
     if (rc) return rc;
     if (lyap) {
       rc = conj_transpose<Hh>(m, m, w.SA, m, w.SB, n, st);
-    } else {
+    } else if (!b_beside) {
       rc = gemm<Hh>('C', 'N', n, n, n, Hh(1), w.QB, n, B, ldb, Hh(0), w.tmp, n, st);
       if (!rc) rc = gemm<Hh>('N', 'N', n, n, n, Hh(1), w.tmp, n, w.QB, n, Hh(0), w.SB, n, st);
     }
