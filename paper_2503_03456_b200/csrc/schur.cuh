@@ -110,7 +110,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
   MSY_SMEM_ATTR_ONCE(apply_z_kernel<S>, (int)applyz_smem<S>(W));
   MSY_SMEM_ATTR_ONCE(apply_z_multi_kernel<S>, (int)applyz_smem<S>(W));
   MSY_SMEM_ATTR_ONCE(apply_z_cl_kernel<S>, (int)azc_smem<S>());
-  static const int azc_mode = getenv("MSY_AZC") ? atoi(getenv("MSY_AZC")) : 1;
+  static const int azc_mode = getenv("MSY_AZC") ? atoi(getenv("MSY_AZC")) : 2;
   if (K < 1 || K > KMAX) return -5;
   const int span = hi - lo;
   const long Tn = 4L * (nb - 1) + span;

@@ -544,7 +544,7 @@ int bs_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb, co
   const int m = p->m, n = p->n;
   Arena ar(wsp, wsb);
   SolveWs<Hh, Hh> w;
-  SolveWs<Hh, Hh>::carve(ar, m, n, p->kind, SYLV_VARIANT_ORTH, w);
+  SolveWs<Hh, Hh>::carve(ar, m, n, p->kind, p->variant, w);  // same carve as sylv_workspace_size
   if (!ar.ok()) return SYLV_EWORKSPACE;
   int rc = ctx_init();
   if (rc) return rc;
