@@ -556,7 +556,7 @@ def run_c4(args):
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded Philox, entropy seed+index)",
             "config": {"workload": f"c4: {total} x real general m=n={m}, mp_orth binary32/binary64, the whole "
                                    f"batch per step, sharded by equation index + gather of X to rank 0",
-                       "m": m, "n": m, "batch": total, "per_rank": cnt, "lanes": args.lanes or 32,
+                       "m": m, "n": m, "batch": total, "per_rank": cnt, "lanes": args.lanes or 64,
                        "iterations": ks, "failed": st_bad, "max_backward_error": be,
                        "lane_phase_ms_mean": {f: round(sum(getattr(r, "ms_" + f) for r in reps) / len(reps), 2)
                                               for f in ("schur", "orth", "setup", "y0", "refine", "recover",

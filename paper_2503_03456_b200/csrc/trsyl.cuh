@@ -146,7 +146,7 @@ template <class S>
 __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
                                                          const S* __restrict__ TB, int ldb, int lowerB, S* W, int ldw,
                                                          const int* __restrict__ rb, const int* __restrict__ cb, int nbi,
-                                                         int nbj, int d, int* status) {
+                                                         int nbj, int d, int* status, int dbg) {
   constexpr int NB = TrsylCfg<S>::NB;
   constexpr int P = 4 * ((NB + 1 + 3) / 4);  // padded tile edge (smem stride)
   constexpr int TG = 16;                     // 16 x 16 threads, RM x RM accumulators each
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
   };
 
   // ---- updates from diagonal d-1 ----
-  if (d >= 1) {
+  if (d >= 1 && !(dbg & 2)) {
     // A-part: W -= TA[I, I*] Y[I*, J], with rank(I*) = d-1-cJ
     int ra = d - 1 - cJ;
     if (ra >= 0 && ra < rI) {
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
     }
   }
   // ---- write back the updated W (or stage it for the leaf solve) ----
-  const bool solve = (dd == d);
+  const bool solve = (dd == d) && !(dbg & 1);  // dbg: timing experiments only (MSY_TRSYL_DBG)
   {
 #pragma unroll
     for (int x = 0; x < RM; x++) {
@@ -591,6 +591,7 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
           int* status, cudaStream_t st) {
   constexpr int NB = TrsylCfg<S>::NB;
   MSY_SMEM_ATTR_ONCE(trsyl_step_kernel<S>, (int)trsyl_smem<S>());
+  static const int dbg = getenv("MSY_TRSYL_DBG") ? atoi(getenv("MSY_TRSYL_DBG")) : 0;
   const int nbi = cdiv(m, NB), nbj = cdiv(n, NB);
   trsyl_partition_kernel<S><<<cdiv(max(nbi, nbj) + 1, 128), 128, 0, st>>>(m, TA, lda, n, TB, ldb, lowerB, NB, w.rb,
                                                                           nbi, w.cb, nbj);
@@ -606,7 +607,7 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
     if (cnt == 0) continue;
     KScope ks(KC_TRSYL, 0, st);
     trsyl_step_kernel<S><<<(unsigned)cnt, TRS_TPB, trsyl_smem<S>(), st>>>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb, w.cb,
-                                                                      nbi, nbj, d, status);
+                                                                      nbi, nbj, d, status, dbg);
     MSY_LAUNCH_CK();
   }
   return 0;
