@@ -13,7 +13,7 @@ import os
 from .errors import DeviceError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmpsylv_b200.so")
+LIB_PATH = os.environ.get("MSY_LIB_PATH") or os.path.join(HERE, "libmpsylv_b200.so")  # override: A/B builds
 
 OK, SINGULAR_EQUATION, NUMERIC_BREAKDOWN, ITERATION_LIMIT = 0, 1, 2, 3
 RANK_DEFICIENT, SINGULAR_MATRIX, FORMAT_OVERFLOW, NON_CONVERGENCE = 4, 5, 6, 7

@@ -22,7 +22,15 @@
 namespace msy {
 
 template <class S> struct MsCfg;
-template <> struct MsCfg<float> { static constexpr int W = 160, NB = 24; };
+#ifndef MSY_FW
+#define MSY_FW 128  // fp32 chase window (compile-time smem layout); MSY_FNB bulges per chain.
+                    // Measured at m=4096: (160,24) 760-825 ms, (128,16) 670, (128,12) 703, (144,20) 750;
+                    // W must be >= the one-CTA block order (128): endgame blocks go through apply_z
+#endif
+#ifndef MSY_FNB
+#define MSY_FNB 16
+#endif
+template <> struct MsCfg<float> { static constexpr int W = MSY_FW, NB = MSY_FNB; };
 template <> struct MsCfg<double> { static constexpr int W = 112, NB = 16; };
 template <> struct MsCfg<cfloat> { static constexpr int W = 112, NB = 16; };
 template <> struct MsCfg<cdouble> { static constexpr int W = 80, NB = 10; };
