@@ -257,9 +257,17 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
   int* ovf_b = ovf + 1;
   SweepCtx* scb = &g_ctx.swB;
   const bool blocking = host_sync_blocking();
+  int nsm = 0;
+  MSY_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  struct CapGuard {  // half the SMs per Hessenberg panel grid while the pair runs
+    int old;
+    explicit CapGuard(int c) : old(hess_grid_cap()) { hess_grid_cap() = c; }
+    ~CapGuard() { hess_grid_cap() = old; }
+  } cap_a(nsm / 2);
   std::thread tb([&]() {
     cudaSetDevice(dev);
     host_sync_blocking() = blocking;
+    hess_grid_cap() = nsm / 2;
     rcb = convert<Ll, Hh>(n, n, B, ldb, w.TB, n, ovf_b, side);
     if (!rcb) rcb = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, side, sb, scb);
     if (!rcb && post_b && sb->status == 0) rcb = (*post_b)(side);
