@@ -109,3 +109,34 @@ def test_golden_fixture_inputs_follow_generators(golden_solves):
     s = golden_solves
     p = P.make("c0", 24, 20, seed=1)
     assert np.array_equal(s["c0_24x20_A"], p.A) and np.array_equal(s["c0_24x20_C"], p.C)
+
+
+def test_bartels_stewart_variant_params_without_gpu():
+    """SYLV_VARIANT_BS: binary64 only (EUNSUPPORTED for low_bits 32); its workspace is the
+    mp_orth one minus the B-side scratch the orth variant runs beside Schur(A)."""
+    from paper_2503_03456_b200 import _native
+    L = _native.lib()
+
+    def size(variant, low_bits, kind=_native.KIND_GENERAL):
+        p = _native.Params(m=300, n=200, kind=kind, complex_data=0, variant=variant, low_bits=low_bits,
+                           correction_bits=64, max_iter=20, y0_zero=0, epsilon=0.0)
+        sz = ct.c_size_t()
+        return L.sylv_workspace_size(ct.byref(p), ct.byref(sz)), sz.value
+
+    rc, bs = size(_native.VARIANT_BS, 64)
+    assert rc == 0 and bs > 0
+    assert size(_native.VARIANT_BS, 32)[0] == _native.EUNSUPPORTED
+    rc, orth64 = size(_native.VARIANT_ORTH, 64)
+    assert rc == 0 and orth64 > bs  # orth(B) + S_B scratch (2 n^2 doubles) beside the A side
+    assert orth64 - bs >= 2 * 200 * 200 * 8
+
+
+def test_kernel_timer_abi_without_gpu():
+    from paper_2503_03456_b200 import _native
+    L = _native.lib()
+    n = 8
+    c, ms, fl = (ct.c_longlong * n)(), (ct.c_double * n)(), (ct.c_double * n)()
+    assert L.sylv_ktimer(1, n, c, ms, fl) == 0
+    assert L.sylv_ktimer(2, n, c, ms, fl) == 0 and sum(c) == 0
+    assert L.sylv_ktimer(0, n, c, ms, fl) == 0
+    assert L.sylv_ktimer(7, n, c, ms, fl) == _native.EINVAL
