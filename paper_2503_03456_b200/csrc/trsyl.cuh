@@ -307,7 +307,39 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
   // sub-tile of row rank a (from the bottom) / column rank b (solve order)
   auto rows_of = [&](int a, int& r0, int& r1) { const int I = nsr - 1 - a; r0 = sr[I]; r1 = sr[I + 1]; };
   auto cols_of = [&](int bb, int& c0, int& c1) { const int J = lowerB ? nsc - 1 - bb : bb; c0 = sc[J]; c1 = sc[J + 1]; };
-  __shared__ int u_of[NWARP][2][LSM + 1], u_len[NWARP][2][LSM + 1], u_rank[NWARP][2][LSM + 1], u_n[NWARP][2];
+  // unit tables of the whole leaf, built once: row units ranked from the bottom, column
+  // units in solve order; a sub-tile's units are a contiguous rank range (edges never
+  // split a 2x2 block)
+  __shared__ int g_rrk[NB + 2], g_rof[NB + 2], g_rln[NB + 2], g_crk[NB + 2], g_cof[NB + 2], g_cln[NB + 2];
+  if (tid == 0) {
+    int cnt = 0, i = bi - 1;
+    while (i >= 0) {
+      const int st2 = (i > 0 && !iszero(As[i + (i - 1) * P])) ? i - 1 : i;
+      for (int q = st2; q <= i; q++) g_rrk[q] = cnt;
+      g_rof[cnt] = st2; g_rln[cnt] = i - st2 + 1; cnt++;
+      i = st2 - 1;
+    }
+  } else if (tid == 32) {
+    int cnt = 0;
+    if (!lowerB) {
+      int j = 0;
+      while (j < bj) {
+        const int len = (j + 1 < bj && !iszero(Bs[(j + 1) + j * P])) ? 2 : 1;
+        for (int q = j; q < j + len; q++) g_crk[q] = cnt;
+        g_cof[cnt] = j; g_cln[cnt] = len; cnt++;
+        j += len;
+      }
+    } else {
+      int j = bj - 1;
+      while (j >= 0) {
+        const int st2 = (j > 0 && !iszero(Bs[(j - 1) + j * P])) ? j - 1 : j;
+        for (int q = st2; q <= j; q++) g_crk[q] = cnt;
+        g_cof[cnt] = st2; g_cln[cnt] = j - st2 + 1; cnt++;
+        j = st2 - 1;
+      }
+    }
+  }
+  __syncthreads();
   for (int s = 0; s < nsr + nsc - 1; s++) {
     // ---- solve the sub-tiles on anti-diagonal s (one warp each) ----
     const int alo = max(0, s - (nsc - 1)), ahi = min(s, nsr - 1);
@@ -317,39 +349,10 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
       rows_of(a, r0, r1);
       cols_of(bb, c0, c1);
       const int ri = r1 - r0, cj = c1 - c0;
-      int* rof = u_of[warp][0]; int* rln = u_len[warp][0]; int* rrk = u_rank[warp][0];
-      int* cof = u_of[warp][1]; int* cln = u_len[warp][1]; int* crk = u_rank[warp][1];
-      if (lane == 0) {
-        int cnt = 0, i = r1 - 1;  // row units from the bottom
-        while (i >= r0) {
-          const int st2 = (i > r0 && !iszero(As[i + (i - 1) * P])) ? i - 1 : i;
-          for (int q = st2; q <= i; q++) rrk[q - r0] = cnt;
-          rof[cnt] = st2; rln[cnt] = i - st2 + 1; cnt++;
-          i = st2 - 1;
-        }
-        u_n[warp][0] = cnt;
-        cnt = 0;
-        if (!lowerB) {
-          int j = c0;
-          while (j < c1) {
-            const int len = (j + 1 < c1 && !iszero(Bs[(j + 1) + j * P])) ? 2 : 1;
-            for (int q = j; q < j + len; q++) crk[q - c0] = cnt;
-            cof[cnt] = j; cln[cnt] = len; cnt++;
-            j += len;
-          }
-        } else {
-          int j = c1 - 1;
-          while (j >= c0) {
-            const int st2 = (j > c0 && !iszero(Bs[(j - 1) + j * P])) ? j - 1 : j;
-            for (int q = st2; q <= j; q++) crk[q - c0] = cnt;
-            cof[cnt] = st2; cln[cnt] = j - st2 + 1; cnt++;
-            j = st2 - 1;
-          }
-        }
-        u_n[warp][1] = cnt;
-      }
-      __syncwarp();
-      const int nru = u_n[warp][0], ncu = u_n[warp][1];
+      const int rbase = g_rrk[r1 - 1], cbase = lowerB ? g_crk[c1 - 1] : g_crk[c0];
+      const int* rof = g_rof + rbase; const int* rln = g_rln + rbase;
+      const int* cof = g_cof + cbase; const int* cln = g_cln + cbase;
+      const int nru = g_rrk[r0] - rbase + 1, ncu = (lowerB ? g_crk[c0] : g_crk[c1 - 1]) - cbase + 1;
       constexpr int EPL = (LSM * LSM + 31) / 32;
       int ei[EPL], ej[EPL], era[EPL], ecr[EPL];
 #pragma unroll
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
         const int e = lane + 32 * k;
         if (e < ri * cj) {
           ei[k] = r0 + e % ri; ej[k] = c0 + e / ri;
-          era[k] = rrk[ei[k] - r0]; ecr[k] = crk[ej[k] - c0];
+          era[k] = g_rrk[ei[k]] - rbase; ecr[k] = g_crk[ej[k]] - cbase;
         } else {
           ei[k] = 0; ej[k] = 0; era[k] = -1000000; ecr[k] = -1000000;
         }

@@ -1,0 +1,12 @@
+# measurement set for the committed state: bench lines + bounded ncu launch list + ncu full
+# capture of the dominant kernel classes (cluster Z application, chase, fp64 GEMM)
+timeout 900 python bench.py > gpurun_out/f_bench_ch.json 2> gpurun_out/f_bench_ch.err; echo "ch $?"
+timeout 900 python bench.py --variant bs --no-cpu-baseline > gpurun_out/f_bench_bs.json 2>/dev/null; echo "bs $?"
+timeout 900 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/f_bench_c4.json 2>/dev/null; echo "c4 $?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 30000 --csv --log-file gpurun_out/f_launches_solve.csv python tools/solve_once.py ch 4096 4096 1 > gpurun_out/f_ncu_list.log 2>&1; echo "ncu list $?"
+timeout 900 ncu --set full --clock-control none -k regex:apply_z_cl --launch-skip 400 -c 6 -o /tmp/ncu_azc python tools/solve_once.py ch 4096 4096 1 > gpurun_out/f_ncu_azc.log 2>&1; echo "ncu azc $?"
+ncu -i /tmp/ncu_azc.ncu-rep --page raw --csv > gpurun_out/f_ncu_azc_raw.csv 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:chase_kernel --launch-skip 200 -c 2 -o /tmp/ncu_ch python tools/solve_once.py ch 4096 4096 1 > gpurun_out/f_ncu_ch.log 2>&1; echo "ncu chase $?"
+ncu -i /tmp/ncu_ch.ncu-rep --page raw --csv > gpurun_out/f_ncu_ch_raw.csv 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:gemm_dmma_kernel --launch-skip 5 -c 2 -o /tmp/ncu_dm2 python tools/solve_once.py ch 4096 4096 1 > gpurun_out/f_ncu_dm.log 2>&1; echo "ncu dm $?"
+ncu -i /tmp/ncu_dm2.ncu-rep --page raw --csv > gpurun_out/f_ncu_dm_raw.csv 2>&1

@@ -1,0 +1,3 @@
+for t in f32 f64; do timeout 300 python tools/trsyl_only.py 4096 $t 3; done
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 600 python tools/probe.py big 2>&1 | grep -v "^schur"
