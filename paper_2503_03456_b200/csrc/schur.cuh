@@ -16,6 +16,7 @@
 
 #include <chrono>
 #include <cstdlib>
+#include <vector>
 
 namespace msy {
 
@@ -30,6 +31,8 @@ struct SchurWs {
   R* shifts;  // 4 per bulge
   int* dinfo; // small device ints
   S* vaed;    // AED window Schur vectors
+  S* Zend;    // Schur vectors of the endgame blocks (sum of block orders^2 <= NMAX * m)
+  int* dend;  // their [status, sweeps] words
   static void carve(Arena& ar, int m, SchurWs& w) {
     if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
     w.Z = ar.get<S>((size_t)2 * KMAX * ZMAX * ZMAX);
@@ -39,6 +42,8 @@ struct SchurWs {
     w.shifts = ar.get<R>(4 * 128);
     w.dinfo = ar.get<int>(64);
     w.vaed = m > SmallCfg<S>::NMAX ? ar.get<S>((size_t)AedCfg<S>::NW * AedCfg<S>::NW) : nullptr;
+    w.Zend = m > SmallCfg<S>::NMAX ? ar.get<S>((size_t)SmallCfg<S>::NMAX * (m + SmallCfg<S>::NMAX)) : nullptr;
+    w.dend = m > SmallCfg<S>::NMAX ? ar.get<int>(2 * (size_t)(m + 1)) : nullptr;
   }
 };
 
@@ -70,16 +75,20 @@ struct PhaseTimer {
 // for direct sylv_schur calls, by the calling host thread.
 struct SweepCtx {
   cudaStream_t aux = nullptr;  // nullptr: serial mode (everything on the caller's stream)
-  cudaEvent_t evC = nullptr, evN = nullptr, evD = nullptr;
+  cudaStream_t eg = nullptr;   // endgame blocks (one-CTA Schur + row-side Z), beside the sweeps
+  cudaEvent_t evC = nullptr, evN = nullptr, evD = nullptr, evE0 = nullptr, evE1 = nullptr;
   int dev = -1;
   void ensure() {
     int d = 0;
     cudaGetDevice(&d);
     if (aux != nullptr && dev == d) return;
     cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&eg, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&evC, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&evN, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&evD, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evE0, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evE1, cudaEventDisableTiming);
     dev = d;
   }
 };
@@ -306,6 +315,16 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
   pt.lap(&loc.ms_hess);
   int hi = m - 1, stag = 0, last_hi = m;
   const int limit = 30 * m;
+  // Endgame blocks (order <= NMAX split off below the active block) are solved beside the
+  // sweeps on the endgame stream: their one-CTA Schur, the row-side Z (H rows of the block,
+  // columns to its right) and U run at once; the column-side update (rows above the block)
+  // is deferred to the end.  Sweeps only multiply rows above the block from the left, so the
+  // deferred right multiplication commutes with them and no entry is written concurrently.
+  static const bool sync_end = getenv("MSY_SYNC_ENDGAME") != nullptr;
+  const bool async_end = sc->aux != nullptr && sc->eg != nullptr && !sync_end && w.Zend != nullptr;
+  struct Deferred { int lo, sz; size_t zoff; };
+  std::vector<Deferred> defs;
+  size_t zoff = 0;
   while (true) {
     scan_kernel<S><<<1, 1024, 0, st>>>(m, A, lda, U, ldu, hi, w.dinfo);
     MSY_LAUNCH_CK();
@@ -318,6 +337,24 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     if (hi < 0) break;
     if (hi < last_hi) { stag = 0; last_hi = hi; } else stag++;
     int sz = hi - lo + 1;
+    if (sz <= NMIN && async_end) {
+      S* blk = A + lo + (size_t)lo * lda;
+      S* Zb = w.Zend + zoff;
+      MSY_CK(cudaEventRecord(sc->evE0, st));
+      MSY_CK(cudaStreamWaitEvent(sc->eg, sc->evE0, 0));
+      rc = schur_small_launch<S>(sz, blk, lda, Zb, sz, SS_WANTZ, nullptr, nullptr, w.dend + 2 * defs.size(), sc->eg);
+      if (rc) return rc;
+      rc = apply_z_regions<S>(m, sz, Zb, A, lda, U, ldu, lo, lo + sz, m, 0, sc->eg);  // rows right + U
+      if (rc) return rc;
+      defs.push_back({lo, sz, zoff});
+      zoff += (size_t)sz * sz;
+      loc.small_calls++;
+      hi = lo - 1;
+      last_hi = hi + 1;
+      stag = 0;
+      if (hi < 0) break;
+      continue;
+    }
     if (sz <= NMIN) {
       S* blk = A + lo + (size_t)lo * lda;
       rc = schur_small_launch<S>(sz, blk, lda, w.Z, sz, SS_WANTZ, nullptr, nullptr, w.dinfo + 8, st);
@@ -423,6 +460,26 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     pt.lap(&loc.ms_sweep);
     loc.sweeps++;
     loc.ms_sweeps++;
+  }
+  if (!defs.empty()) {  // join the endgame stream, apply the deferred column sides, read statuses
+    MSY_CK(cudaEventRecord(sc->evE1, sc->eg));
+    MSY_CK(cudaStreamWaitEvent(st, sc->evE1, 0));
+    for (const Deferred& d : defs) {
+      if (d.lo == 0) continue;
+      rc = apply_z_regions<S>(m, d.sz, w.Zend + d.zoff, A, lda, nullptr, ldu, d.lo, 0, 0, d.lo, st);
+      if (rc) return rc;
+    }
+    const size_t nd = defs.size();
+    for (size_t k0 = 0; k0 < nd; k0 += 500) {
+      const size_t cnt = std::min<size_t>(500, nd - k0);
+      int hs[1000];
+      MSY_CK(d2h(hs, w.dend + 2 * k0, 2 * cnt * sizeof(int), st));
+      for (size_t k = 0; k < cnt; k++) {
+        loc.sweeps += hs[2 * k + 1];
+        if (hs[2 * k] && !loc.status) loc.status = hs[2 * k];
+      }
+    }
+    pt.lap(&loc.ms_small);
   }
   if (stats) *stats = loc;
   return 0;
