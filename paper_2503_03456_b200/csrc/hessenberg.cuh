@@ -25,7 +25,10 @@ namespace cg = cooperative_groups;
 
 namespace msy {
 
-constexpr int HESS_NB = 32;     // panel width
+#ifndef MSY_HESS_NB
+#define MSY_HESS_NB 32  // the panel kernels assume 32 (one lane per panel column): other widths are not supported
+#endif
+constexpr int HESS_NB = MSY_HESS_NB;  // panel width
 constexpr int HESS_CHUNK = 64;  // gemv column chunk
 constexpr int HESS_ROWS = 128;  // gemv rows per CTA
 constexpr int HESS_TPB = 512;
