@@ -53,40 +53,64 @@ __global__ void __launch_bounds__(256) potrf_small_kernel(int nb, S* G, int ldg,
   }
 }
 
-// Solve R^H X = B in place (R nb x nb upper => R^H lower), B is nb x ncols
+// Solve R^H X = B in place (R nb x nb upper => R^H lower), B is nb x ncols.  One thread per
+// column; the substitution is fully unrolled over the compile-time block edge so the column
+// stays in registers, and the pivots are applied as precomputed reciprocals.
 template <class S>
-__global__ void __launch_bounds__(256) trsm_lhu_kernel(int nb, const S* Rk, int ldr, int ncols, S* B, int ldb) {
-  __shared__ S Rs[ChNb<S>::v][ChNb<S>::v + 1];
+__global__ void __launch_bounds__(128) trsm_lhu_kernel(int nb, const S* Rk, int ldr, int ncols, S* B, int ldb) {
+  constexpr int NB = ChNb<S>::v;
+  __shared__ S Rs[NB][NB + 1];
+  __shared__ S rinv[NB];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) Rs[e % nb][e / nb] = Rk[(e % nb) + (size_t)(e / nb) * ldr];
   __syncthreads();
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) rinv[i] = S(1) / conj(Rs[i][i]);
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncols) return;
-  S x[ChNb<S>::v];
-  for (int i = 0; i < nb; i++) x[i] = B[i + (size_t)c * ldb];
-  for (int i = 0; i < nb; i++) {
-    S s = x[i];
-    for (int q = 0; q < i; q++) s = s - conj(Rs[q][i]) * x[q];
-    x[i] = s / conj(Rs[i][i]);
+  S x[NB];
+#pragma unroll
+  for (int i = 0; i < NB; i++) x[i] = i < nb ? B[i + (size_t)c * ldb] : S(0);
+#pragma unroll
+  for (int i = 0; i < NB; i++) {
+    if (i < nb) {
+      S s = x[i];
+#pragma unroll
+      for (int q = 0; q < i; q++) s = s - conj(Rs[q][i]) * x[q];
+      x[i] = s * rinv[i];
+    }
   }
-  for (int i = 0; i < nb; i++) B[i + (size_t)c * ldb] = x[i];
+#pragma unroll
+  for (int i = 0; i < NB; i++)
+    if (i < nb) B[i + (size_t)c * ldb] = x[i];
 }
 
-// Solve X R = B in place (R nb x nb upper), B is nrows x nb
+// Solve X R = B in place (R nb x nb upper), B is nrows x nb (one thread per row, unrolled)
 template <class S>
 __global__ void __launch_bounds__(128) trsm_rup_kernel(int nb, const S* Rk, int ldr, int nrows, S* B, int ldb) {
-  __shared__ S Rs[ChNb<S>::v][ChNb<S>::v + 1];
+  constexpr int NB = ChNb<S>::v;
+  __shared__ S Rs[NB][NB + 1];
+  __shared__ S rinv[NB];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) Rs[e % nb][e / nb] = Rk[(e % nb) + (size_t)(e / nb) * ldr];
   __syncthreads();
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) rinv[i] = S(1) / Rs[i][i];
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
-  S x[ChNb<S>::v];
-  for (int j = 0; j < nb; j++) x[j] = B[r + (size_t)j * ldb];
-  for (int j = 0; j < nb; j++) {
-    S s = x[j];
-    for (int q = 0; q < j; q++) s = s - x[q] * Rs[q][j];
-    x[j] = s / Rs[j][j];
+  S x[NB];
+#pragma unroll
+  for (int j = 0; j < NB; j++) x[j] = j < nb ? B[r + (size_t)j * ldb] : S(0);
+#pragma unroll
+  for (int j = 0; j < NB; j++) {
+    if (j < nb) {
+      S s = x[j];
+#pragma unroll
+      for (int q = 0; q < j; q++) s = s - x[q] * Rs[q][j];
+      x[j] = s * rinv[j];
+    }
   }
-  for (int j = 0; j < nb; j++) B[r + (size_t)j * ldb] = x[j];
+#pragma unroll
+  for (int j = 0; j < NB; j++)
+    if (j < nb) B[r + (size_t)j * ldb] = x[j];
 }
 
 template <class S>
@@ -109,7 +133,7 @@ int orth_cholqr(int m, const S* U, int ldu, S* Q, int ldq, S* G, int ldg, int* d
     int rest = m - k - nb;
     if (rest > 0) {
       S* Gkr = G + k + (size_t)(k + nb) * ldg;
-      trsm_lhu_kernel<S><<<cdiv(rest, 256), 256, 0, st>>>(nb, Gkk, ldg, rest, Gkr, ldg);
+      trsm_lhu_kernel<S><<<cdiv(rest, 128), 128, 0, st>>>(nb, Gkk, ldg, rest, Gkr, ldg);
       MSY_LAUNCH_CK();
       rc = gemm<S>('C', 'N', rest, rest, nb, S(-1), Gkr, ldg, Gkr, ldg, S(1), G + (k + nb) + (size_t)(k + nb) * ldg, ldg,
                    st);
