@@ -22,8 +22,11 @@ namespace msy {
 
 // LEAF2: two-level leaf (sub-tile wavefront); measured faster for the 64-wide leaves,
 // slower for the 32-wide complex128 leaves, which keep the single-level wavefront
-template <class S> struct TrsylCfg { static constexpr int NB = 64; static constexpr bool LEAF2 = true; };
-template <> struct TrsylCfg<cdouble> { static constexpr int NB = 32; static constexpr bool LEAF2 = false; };
+// LEAF: 3 = lazy single-warp element wavefront (each unit gathers its row / column dot
+// products when it becomes ready: ~nru + ncu warp-synchronous steps, no block barriers);
+// 2 = two-level sub-tile wavefront; 1 = eager single-level wavefront (block barriers)
+template <class S> struct TrsylCfg { static constexpr int NB = 64; static constexpr int LEAF = 3; };
+template <> struct TrsylCfg<cdouble> { static constexpr int NB = 32; static constexpr int LEAF = 3; };
 
 enum { TRS_OK = 0, TRS_SINGULAR = 1, TRS_BREAKDOWN = 2 };
 
@@ -263,7 +266,118 @@ __global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, co
     }
   }
   if (!solve) return;
-  if constexpr (TrsylCfg<S>::LEAF2) {
+  if constexpr (TrsylCfg<S>::LEAF == 3) {
+    for (int e = tid; e < bi * bi; e += nt) {
+      int i = e % bi, k = e / bi;
+      As[i + k * P] = TA[(i0 + i) + (size_t)(i0 + k) * lda];
+    }
+    for (int e = tid; e < bj * bj; e += nt) {
+      int i = e % bj, k = e / bj;
+      Bs[i + k * P] = TB[(j0 + i) + (size_t)(j0 + k) * ldb];
+    }
+    __syncthreads();
+    __shared__ int g_rof[NB + 2], g_rln[NB + 2], g_cof[NB + 2], g_cln[NB + 2], g_n[2];
+    if (tid == 0) {  // row units from the bottom
+      int cnt = 0, i = bi - 1;
+      while (i >= 0) {
+        const int st2 = (i > 0 && !iszero(As[i + (i - 1) * P])) ? i - 1 : i;
+        g_rof[cnt] = st2; g_rln[cnt] = i - st2 + 1; cnt++;
+        i = st2 - 1;
+      }
+      g_n[0] = cnt;
+    } else if (tid == 32) {  // column units in solve order
+      int cnt = 0;
+      if (!lowerB) {
+        int j = 0;
+        while (j < bj) {
+          const int len = (j + 1 < bj && !iszero(Bs[(j + 1) + j * P])) ? 2 : 1;
+          g_cof[cnt] = j; g_cln[cnt] = len; cnt++;
+          j += len;
+        }
+      } else {
+        int j = bj - 1;
+        while (j >= 0) {
+          const int st2 = (j > 0 && !iszero(Bs[(j - 1) + j * P])) ? j - 1 : j;
+          g_cof[cnt] = st2; g_cln[cnt] = j - st2 + 1; cnt++;
+          j = st2 - 1;
+        }
+      }
+      g_n[1] = cnt;
+    }
+    __syncthreads();
+    if (warp < 2) {  // two warps run the wavefront, synchronised by a 64-thread named barrier
+      const int nru = g_n[0], ncu = g_n[1];
+      for (int s = 0; s < nru + ncu - 1; s++) {
+        for (int a = tid; a < nru; a += 64) {
+          const int bb = s - a;
+          if (bb < 0 || bb >= ncu) continue;
+          const int iu = g_rof[a], p = g_rln[a], ju = g_cof[bb], q = g_cln[bb];
+          const int kb = iu + p;                                        // rows below the unit
+          const int la = lowerB ? ju + q : 0, lb = lowerB ? bj : ju;   // columns solved before it
+          // one fused walk over both dot products: x stride P, y stride 1 in both pieces
+          const int nr = bi - kb, tot = nr + (lb - la);
+          const S* xa = As + iu + (size_t)kb * P;          // t <  nr: As[iu, kb + t]
+          const S* xb = Ws + iu + (ptrdiff_t)(la - nr) * P;  // t >= nr: Ws[iu, la + t - nr]
+          const S* ya = Ws + kb + (size_t)ju * P;          // t <  nr: Ws[kb + t, ju]
+          const S* yb = Bs + (la - nr) + (size_t)ju * P;   // t >= nr: Bs[la + t - nr, ju]
+          bool ok = true;
+          if (p == 1 && q == 1) {
+            S v0 = Ws[iu + ju * P], v1 = S(0), v2 = S(0), v3 = S(0);
+            int t = 0;
+            for (; t + 3 < tot; t += 4) {
+#pragma unroll
+              for (int u = 0; u < 4; u++) {
+                const int tt = t + u;
+                const S* X = tt < nr ? xa : xb;
+                const S* Y = tt < nr ? ya : yb;
+                const S prod = X[(size_t)tt * P] * Y[tt];
+                if (u == 0) v0 = v0 - prod; else if (u == 1) v1 = v1 - prod; else if (u == 2) v2 = v2 - prod; else v3 = v3 - prod;
+              }
+            }
+            for (; t < tot; t++) {
+              const S* X = t < nr ? xa : xb;
+              const S* Y = t < nr ? ya : yb;
+              v0 = v0 - X[(size_t)t * P] * Y[t];
+            }
+            const S dd = As[iu + iu * P] + Bs[ju + ju * P];
+            ok = !iszero(dd);
+            Ws[iu + ju * P] = ok ? ((v0 + v1) + (v2 + v3)) * (S(1) / dd) : mk<S>(NAN, NAN);
+          } else {
+            S v00 = Ws[iu + ju * P];
+            S v10 = p > 1 ? Ws[(iu + 1) + ju * P] : S(0);
+            S v01 = q > 1 ? Ws[iu + (ju + 1) * P] : S(0);
+            S v11 = (p > 1 && q > 1) ? Ws[(iu + 1) + (ju + 1) * P] : S(0);
+            const int di = p > 1 ? 1 : 0, dj = q > 1 ? (int)P : 0;  // duplicates are discarded
+            for (int t = 0; t < tot; t++) {
+              const S* X = t < nr ? xa : xb;
+              const S* Y = t < nr ? ya : yb;
+              const size_t xo = (size_t)t * P;
+              const S a0 = X[xo], a1 = X[xo + di], y0 = Y[t], y1 = Y[t + dj];
+              v00 = v00 - a0 * y0; v10 = v10 - a1 * y0; v01 = v01 - a0 * y1; v11 = v11 - a1 * y1;
+            }
+            Ws[iu + ju * P] = v00;
+            if (p > 1) Ws[(iu + 1) + ju * P] = v10;
+            if (q > 1) Ws[iu + (ju + 1) * P] = v01;
+            if (p > 1 && q > 1) Ws[(iu + 1) + (ju + 1) * P] = v11;
+            if (p == 2 && q == 1) ok = unit_solve<S, 2, 1>(As, Bs, Ws, P, iu, ju);
+            else if (p == 1 && q == 2) ok = unit_solve<S, 1, 2>(As, Bs, Ws, P, iu, ju);
+            else ok = unit_solve<S, 2, 2>(As, Bs, Ws, P, iu, ju);
+          }
+          if (!ok) {  // singular diagonal pair: report the first in reference order (decoded on the host)
+            const int jg = j0 + ju, ig = i0 + iu + p - 1;
+            const int crank = lowerB ? (n - 1 - jg) : jg;
+            atomicMin(&status[0], crank * m + (m - 1 - ig));
+          }
+        }
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < bi * bj; e += nt) {
+      int i = e % bi, j = e / bi;
+      W[(i0 + i) + (size_t)(j0 + j) * ldw] = Ws[i + j * P];
+    }
+  } else if constexpr (TrsylCfg<S>::LEAF == 2) {
   // ---- leaf: TA_II Y + Y TB_JJ = W_IJ in shared memory ----
   // Two levels: the leaf is cut into sub-tiles of ~LST x LST (edges nudged so no 2x2
   // block is split); sub-tile anti-diagonals are processed in order.  On each, one

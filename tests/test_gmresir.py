@@ -50,7 +50,11 @@ def test_device_gmres_ir_golden(golden_gmres, tag):
     assert rep.converged == bool(g[f"{tag}_conv"])
     assert abs(rep.outer_iterations - int(g[f"{tag}_outer"])) <= 1
     assert len(rep.inner_iterations) == rep.outer_iterations
-    ref_res = float(g[f"{tag}_hist"][-1])
+    # residual after the same number of outer steps (the counts may differ by one: with
+    # u_g = binary32 the preconditioner's rounding decides whether ||E|| <= eps ||X|| one
+    # step earlier or later)
+    hist = g[f"{tag}_hist"]
+    ref_res = float(hist[min(rep.outer_iterations, len(hist)) - 1])
     assert rep.residual_history[-1] <= 10 * max(ref_res, U64)
     Xr = g[f"{tag}_X"]
     assert np.linalg.norm(rep.X - Xr) / np.linalg.norm(Xr) <= 10 * kappa_sylv(A, B) * U64 * 10
