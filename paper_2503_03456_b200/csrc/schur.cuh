@@ -36,7 +36,7 @@ struct SchurWs {
   static void carve(Arena& ar, int m, SchurWs& w) {
     if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
     w.Z = ar.get<S>((size_t)2 * KMAX * ZMAX * ZMAX);
-    w.sblk = ar.get<S>(192 * 192);
+    w.sblk = ar.get<S>((size_t)EigCfg<S>::NMAX * EigCfg<S>::NMAX);
     w.wr = ar.get<R>(256);
     w.wi = ar.get<R>(256);
     w.shifts = ar.get<R>(4 * 128);

@@ -24,7 +24,10 @@ namespace msy {
 
 template <class S> struct MssCfg { static constexpr int NWARP = 8; };
 // largest order of an eigenvalues-only call (no Z: the smem holds one matrix)
-template <class S> struct EigCfg { static constexpr int NMAX = sizeof(S) == 4 ? 192 : (sizeof(S) == 8 ? 144 : 104); };
+#ifndef MSY_EIGMAX_F32
+#define MSY_EIGMAX_F32 192
+#endif
+template <class S> struct EigCfg { static constexpr int NMAX = sizeof(S) == 4 ? MSY_EIGMAX_F32 : (sizeof(S) == 8 ? 144 : 104); };
 constexpr int MSS_A2 = 33;  // ld of the shift-block scratch (<= 32 x 32 plus dummy row/column)
 
 // Eigenvalues of the k x k upper Hessenberg matrix A (smem, column-major, ld
