@@ -289,16 +289,24 @@ __global__ void __cluster_dims__(Azc<S>::N, 1, 1) __launch_bounds__(AZC_THREADS)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int o0 = part * 32;                 // this CTA's output slice
   const int no = min(32, nz - o0);          // <= 0: nothing to write (still joins the barrier)
-  // slice of Z: columns o0..o0+no-1 (L uses conj(Z[k, o]), R/U use Z[k, o])
-  for (int e = tid; e < nz * 32; e += AZC_THREADS) {
-    const int k = e % nz, o = e / nz;
-    Zc[k * CP + o] = o < no ? Zg[k + (size_t)(o0 + o) * nz] : S(0);
+  static_assert(MsCfg<S>::W <= AZC_THREADS, "one staged row per thread");
+  // slice of Z: columns o0..o0+no-1 (L uses conj(Z[k, o]), R/U use Z[k, o]).  Thread k stages
+  // row k: 32 independent coalesced loads in flight, then 32 shared stores.
+  if (tid < nz) {
+    S v[32];
+#pragma unroll
+    for (int o = 0; o < 32; o++) v[o] = o < no ? Zg[tid + (size_t)(o0 + o) * nz] : S(0);
+#pragma unroll
+    for (int o = 0; o < 32; o++) Zc[tid * CP + o] = v[o];
   }
   if (b < ntL) {  // ---- region L: H[r0 + o, c] <- sum_k conj(Z[k, o]) H[r0 + k, c] ----
     const int c0 = cL0 + b * 32, nc = min(32, cL1 - c0);
-    for (int e = tid; e < nz * 32; e += AZC_THREADS) {
-      const int k = e % nz, c = e / nz;
-      Ts[k * TP + c] = c < nc ? H[(r0 + k) + (size_t)(c0 + c) * ldh] : S(0);
+    if (tid < nz) {
+      S v[32];
+#pragma unroll
+      for (int c = 0; c < 32; c++) v[c] = c < nc ? H[(r0 + tid) + (size_t)(c0 + c) * ldh] : S(0);
+#pragma unroll
+      for (int c = 0; c < 32; c++) Ts[tid * TP + c] = v[c];
     }
     cl.sync();
     if (no > 0) {
@@ -326,9 +334,19 @@ __global__ void __cluster_dims__(Azc<S>::N, 1, 1) __launch_bounds__(AZC_THREADS)
   if (b < ntR) { M = H; ldm = ldh; rbase = rlo + b * 32; nrows = min(32, rR1 - rbase); }
   else { b -= ntR; M = U; ldm = ldu; rbase = b * 32; nrows = min(32, mU - rbase); }
   // ---- regions R / U: M[r, r0 + o] <- sum_k M[r, r0 + k] Z[k, o] ----
-  for (int e = tid; e < nz * 32; e += AZC_THREADS) {
-    const int r = e % 32, k = e / 32;
-    Ts[k * TP + r] = r < nrows ? M[(rbase + r) + (size_t)(r0 + k) * ldm] : S(0);
+  {  // thread (r = lane, k = warp + 4 i): coalesced along r, nz / 4 independent loads per thread
+    constexpr int KI = (MsCfg<S>::W + 3) / 4;
+    S v[KI];
+#pragma unroll
+    for (int i = 0; i < KI; i++) {
+      const int k = warp + 4 * i;
+      v[i] = (k < nz && lane < nrows) ? M[(rbase + lane) + (size_t)(r0 + k) * ldm] : S(0);
+    }
+#pragma unroll
+    for (int i = 0; i < KI; i++) {
+      const int k = warp + 4 * i;
+      if (k < nz) Ts[k * TP + lane] = v[i];
+    }
   }
   cl.sync();
   if (no <= 0) return;
