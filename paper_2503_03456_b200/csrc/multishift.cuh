@@ -382,7 +382,17 @@ int apply_z_regions(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int
   int nblk = (cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
   if (nblk == 0) return 0;
   KScope ks(KC_APPLYZ, (tr<S>::cx ? 8.0 : 2.0) * nz * nz * ((cL1 > cL0 ? cL1 - cL0 : 0) + rR1 + (U ? m : 0)), st);
-  apply_z_kernel<S><<<nblk, 256, applyz_smem<S>(nz), st>>>(nz, Z, H, ldh, w0, cL0, cL1, rR1, U, ldu, U ? m : 0);
+  static const int azc_mode = getenv("MSY_AZC") ? atoi(getenv("MSY_AZC")) : 2;
+  if (azc_mode >= 2) {  // the cluster-split kernel with a single job
+    MSY_SMEM_ATTR_ONCE(apply_z_cl_kernel<S>, (int)azc_smem<S>());
+    ApplyJobs<S> j = {};
+    j.n = 1; j.start[0] = 0; j.start[1] = nblk;
+    j.nz[0] = nz; j.Z[0] = Z; j.r0[0] = w0; j.cL0[0] = cL0; j.cL1[0] = cL1; j.rlo[0] = 0; j.rR1[0] = rR1;
+    j.mU[0] = U ? m : 0;
+    apply_z_cl_kernel<S><<<nblk * Azc<S>::N, AZC_THREADS, azc_smem<S>(), st>>>(H, ldh, U, ldu, j);
+  } else {
+    apply_z_kernel<S><<<nblk, 256, applyz_smem<S>(nz), st>>>(nz, Z, H, ldh, w0, cL0, cL1, rR1, U, ldu, U ? m : 0);
+  }
   MSY_LAUNCH_CK();
   return 0;
 }
