@@ -67,10 +67,26 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
 #define HW(i, j) Hw[(i) + (j) * ld]
 #define ZW(i, j) Zw[(i) + (j) * ld]
-  for (int e = tid; e < nw * nw; e += nt) {
-    int i = e % nw, j = e / nw;
-    HW(i, j) = H[(ws + i) + (size_t)(ws + j) * ldh];
-    ZW(i, j) = (i == j) ? S(1) : S(0);
+  constexpr int WW = MsCfg<S>::W;
+  if (nt % WW == 0 && nt / WW >= 4) {  // thread (row i, column class jc): <= 32 loads in flight
+    const int i = tid % WW, jc = tid / WW, cs = nt / WW;
+    S v[32];
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const int j = jc + cs * k;
+      v[k] = (i < nw && j < nw) ? H[(ws + i) + (size_t)(ws + j) * ldh] : S(0);
+    }
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const int j = jc + cs * k;
+      if (i < nw && j < nw) { HW(i, j) = v[k]; ZW(i, j) = (i == j) ? S(1) : S(0); }
+    }
+  } else {
+    for (int e = tid; e < nw * nw; e += nt) {
+      int i = e % nw, j = e / nw;
+      HW(i, j) = H[(ws + i) + (size_t)(ws + j) * ldh];
+      ZW(i, j) = (i == j) ? S(1) : S(0);
+    }
   }
   __syncthreads();
   const int j = warp;  // bulge handled by this warp
