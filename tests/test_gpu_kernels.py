@@ -164,7 +164,7 @@ def _check_schur(A, sf, u, quasi):
     assert d <= 1e3 * m * u * max(1.0, np.abs(ev).max())
 
 
-@pytest.mark.parametrize("m", [1, 2, 6, 17, 50, 128, 129, 200, 300, 520])
+@pytest.mark.parametrize("m", [1, 2, 6, 17, 50, 128, 129, 200, 300, 520, 1100])
 def test_schur_real_fp32(B200, rng, m):
     from paper_2503_03456_b200 import BINARY32, PrecisionContext
     A = rng.standard_normal((m, m))
@@ -172,7 +172,7 @@ def test_schur_real_fp32(B200, rng, m):
     _check_schur(A, sf, 2.0 ** -24, quasi=True)
 
 
-@pytest.mark.parametrize("m", [6, 50, 96, 97, 260])
+@pytest.mark.parametrize("m", [6, 50, 96, 97, 260, 700])
 def test_schur_complex_fp32(B200, rng, m):
     from paper_2503_03456_b200 import BINARY32, PrecisionContext
     A = cmat(rng, m, m)
@@ -180,13 +180,16 @@ def test_schur_complex_fp32(B200, rng, m):
     _check_schur(A, sf, 2.0 ** -24, quasi=False)
 
 
-@pytest.mark.parametrize("m", [12, 150])
+@pytest.mark.parametrize("m", [12, 150, 400])
 def test_schur_binary64(B200, rng, m):
+    """Real binary64 (one-CTA and multishift paths) and complex binary64 (past its 64 one-CTA
+    limit at 100: multishift with async endgame blocks)."""
     from paper_2503_03456_b200 import BINARY64, PrecisionContext
     A = rng.standard_normal((m, m))
     _check_schur(A, B200.schur(A, PrecisionContext(BINARY64)), 2.0 ** -53, quasi=True)
-    Ac = cmat(rng, 40, 40)
-    _check_schur(Ac, B200.schur(Ac, PrecisionContext(BINARY64)), 2.0 ** -53, quasi=False)
+    for mc in (40, 100):
+        Ac = cmat(rng, mc, mc)
+        _check_schur(Ac, B200.schur(Ac, PrecisionContext(BINARY64)), 2.0 ** -53, quasi=False)
 
 
 def test_schur_reference_kats(B200, rng):
