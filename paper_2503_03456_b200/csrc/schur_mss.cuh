@@ -353,10 +353,24 @@ __global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S
   const R u = tol > R(0) ? tol : tr<S>::u();  // deflation tolerance (looser for shift-only calls)
 #define HH(i, j) H[(i) + (j) * ld]
 #define ZZ(i, j) Zs[(i) + (j) * ld]
-  for (int e = tid; e < n * n; e += nt) {
-    int i = e % n, j = e / n;
-    HH(i, j) = Hg[i + (size_t)j * ldh];
-    if (wantz) ZZ(i, j) = (flags & SS_ZIN) ? Zg[i + (size_t)j * ldz] : (i == j ? S(1) : S(0));
+  if (n <= nt && !(flags & SS_ZIN)) {  // thread i stages row i: 16 independent loads in flight
+    for (int j0 = 0; j0 < n; j0 += 16) {
+      S v[16];
+#pragma unroll
+      for (int u = 0; u < 16; u++) v[u] = (tid < n && j0 + u < n) ? Hg[tid + (size_t)(j0 + u) * ldh] : S(0);
+#pragma unroll
+      for (int u = 0; u < 16; u++)
+        if (tid < n && j0 + u < n) {
+          HH(tid, j0 + u) = v[u];
+          if (wantz) ZZ(tid, j0 + u) = (tid == j0 + u) ? S(1) : S(0);
+        }
+    }
+  } else {
+    for (int e = tid; e < n * n; e += nt) {
+      int i = e % n, j = e / n;
+      HH(i, j) = Hg[i + (size_t)j * ldh];
+      if (wantz) ZZ(i, j) = (flags & SS_ZIN) ? Zg[i + (size_t)j * ldz] : (i == j ? S(1) : S(0));
+    }
   }
   __syncthreads();
   if (flags & SS_HESS) smem_hessenberg<S>(n, H, Zs, ld, wantz, vbuf, sh.bt);
