@@ -510,6 +510,12 @@ __global__ void pair_shifts_kernel(int ns, const typename tr<S>::R* wr, const ty
                                    typename tr<S>::R* out, int exceptional, const S* H, int ldh, int lo, int hi,
                                    int* nb_out) {
   typedef typename tr<S>::R R;
+  // stage the eigenvalues in shared memory first (one dependent global round trip per
+  // element in the serial pairing loop otherwise)
+  __shared__ R swr[256], swi[256];
+  for (int k = threadIdx.x; k < ns && k < 256; k += blockDim.x) { swr[k] = wr[k]; swi[k] = wi[k]; }
+  __syncthreads();
+  if (ns <= 256) { wr = swr; wi = swi; }
   if (threadIdx.x != 0) return;
   int b = 0;
   if (exceptional) {
