@@ -144,9 +144,12 @@ __device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int 
   return ok;
 }
 
+#ifndef MSY_TRS_MINB
+#define MSY_TRS_MINB 2
+#endif
 constexpr int TRS_TPB = 256;  // 2 CTAs per SM: the update of one block overlaps another's loads
 template <class S>
-__global__ void __launch_bounds__(TRS_TPB, 2) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
+__global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
                                                          const S* __restrict__ TB, int ldb, int lowerB, S* W, int ldw,
                                                          const int* __restrict__ rb, const int* __restrict__ cb, int nbi,
                                                          int nbj, int d, int* status, int dbg) {
