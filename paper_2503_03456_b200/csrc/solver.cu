@@ -41,6 +41,8 @@ struct StreamCtx {
   SweepCtx swA, swB;  // aux streams of the two concurrent Schur factorisations
   SweepCtx serial;    // no aux stream: batched lanes run everything on their own stream
   cudaStream_t side = nullptr;
+  cudaStream_t hiA = nullptr;  // Schur(A)'s critical path (high priority; side is Schur(B)'s)
+  cudaEvent_t ev_a = nullptr;
   cudaEvent_t ev_in = nullptr, ev_side = nullptr;
   cudaEvent_t ev[8];
   bool init = false;
@@ -54,7 +56,15 @@ int ctx_init() {
   int dev;
   MSY_CK(cudaGetDevice(&dev));
   if (g_ctx.init && g_ctx.device == dev) return 0;
-  MSY_CK(cudaStreamCreateWithFlags(&g_ctx.side, cudaStreamNonBlocking));
+  // The chase / near-Z / shift kernels of both Schur factorisations run on high-priority
+  // streams; their far Z applications and endgame blocks (SweepCtx aux / eg) keep the
+  // default (least) priority, so queued far work yields SMs to the critical path.
+  int lo_pri = 0, hi_pri = 0;
+  MSY_CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+  static const bool no_pri = getenv("MSY_NO_STREAM_PRIORITY") != nullptr;
+  MSY_CK(cudaStreamCreateWithPriority(&g_ctx.side, cudaStreamNonBlocking, no_pri ? lo_pri : hi_pri));
+  MSY_CK(cudaStreamCreateWithPriority(&g_ctx.hiA, cudaStreamNonBlocking, no_pri ? lo_pri : hi_pri));
+  MSY_CK(cudaEventCreateWithFlags(&g_ctx.ev_a, cudaEventDisableTiming));
   MSY_CK(cudaEventCreateWithFlags(&g_ctx.ev_in, cudaEventDisableTiming));
   MSY_CK(cudaEventCreateWithFlags(&g_ctx.ev_side, cudaEventDisableTiming));
   for (int i = 0; i < 8; i++) MSY_CK(cudaEventCreate(&g_ctx.ev[i]));
@@ -272,10 +282,14 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
     if (!rcb) rcb = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, side, sb, scb);
     if (!rcb && post_b && sb->status == 0) rcb = (*post_b)(side);
   });
-  rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, st, sa, &g_ctx.swA);
+  cudaStream_t sa_st = g_ctx.hiA;  // ev_in (recorded above, after convert(A)) orders it after st
+  MSY_CK(cudaStreamWaitEvent(sa_st, g_ctx.ev_in, 0));
+  rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, sa_st, sa, &g_ctx.swA);
   tb.join();
   if (rc) return rc;
   if (rcb) return rcb;
+  MSY_CK(cudaEventRecord(g_ctx.ev_a, sa_st));
+  MSY_CK(cudaStreamWaitEvent(st, g_ctx.ev_a, 0));
   MSY_CK(cudaEventRecord(g_ctx.ev_side, side));
   MSY_CK(cudaStreamWaitEvent(st, g_ctx.ev_side, 0));
   return 0;
