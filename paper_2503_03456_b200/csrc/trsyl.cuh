@@ -161,22 +161,33 @@ __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m
   // the bottom, cJ = column rank in solve order): rows rI < d with cJ >= d - rI, then
   // columns cJ < d with rI >= d; at d = 0 the single block (0, 0).  Blocks with rI >= d
   // and cJ >= d receive nothing yet and are not launched.
-  int rI, cJ;
+  // The blocks that solve at this step (rank sum d: the leaves, on the critical path) take
+  // the lowest block indices so they are scheduled first and their leaf solves overlap the
+  // update-only waves; the update-only blocks follow in the original order.
+  int rI = 0, cJ = 0;
   {
     int b = blockIdx.x;
-    if (d == 0) { rI = 0; cJ = 0; }
-    else {
-      const int ra = min(d, nbi);
-      rI = -1;
-      for (int r = 0; r < ra; r++) {
-        const int len = max(0, nbj - max(0, d - r));
-        if (b < len) { rI = r; cJ = max(0, d - r) + b; break; }
-        b -= len;
-      }
-      if (rI < 0) {  // second part: columns cJ < d, rows rI >= d
-        const int h = nbi - d;
-        cJ = b / h;
-        rI = d + b % h;
+    if (d > 0) {
+      const int llo = max(0, d - nbj + 1), lhi = min(d, nbi - 1);
+      const int nleaf = max(0, lhi - llo + 1);
+      if (b < nleaf) {
+        rI = llo + b;
+        cJ = d - rI;
+      } else {
+        b -= nleaf;
+        const int ra = min(d, nbi);
+        rI = -1;
+        for (int r = 0; r < ra; r++) {  // row r: blocks cJ in [d - r, nbj), the first is the leaf
+          const int st = (d - r < nbj) ? d - r + 1 : d - r;
+          const int len = max(0, nbj - st);
+          if (b < len) { rI = r; cJ = st + b; break; }
+          b -= len;
+        }
+        if (rI < 0) {  // columns cJ < min(d, nbj), rows rI >= d, without the leaf (d, 0)
+          const int h = nbi - d;
+          if (b < h - 1) { cJ = 0; rI = d + 1 + b; }
+          else { b -= h - 1; cJ = 1 + b / h; rI = d + b % h; }
+        }
       }
     }
   }
