@@ -22,7 +22,10 @@
 
 namespace msy {
 
-template <class S> struct MssCfg { static constexpr int NWARP = 8; };
+#ifndef MSY_MSS_NWARP
+#define MSY_MSS_NWARP 8  // warps (= bulges per sweep) of the one-CTA multishift kernel
+#endif
+template <class S> struct MssCfg { static constexpr int NWARP = MSY_MSS_NWARP; };
 // largest order of an eigenvalues-only call (no Z: the smem holds one matrix)
 #ifndef MSY_EIGMAX_F32
 #define MSY_EIGMAX_F32 192
@@ -327,7 +330,7 @@ struct MssShared {
 };
 
 template <class S, int LDC>
-__global__ void __launch_bounds__(256) schur_mss_kernel(int n, S* Hg, int ldh, S* Zg, int ldz, int flags,
+__global__ void __launch_bounds__(32 * MSY_MSS_NWARP) schur_mss_kernel(int n, S* Hg, int ldh, S* Zg, int ldz, int flags,
                                                        typename tr<S>::R* wr, typename tr<S>::R* wi, int* info,
                                                        typename tr<S>::R tol) {
   typedef typename tr<S>::R R;
