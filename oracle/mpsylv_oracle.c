@@ -42,6 +42,9 @@
 #include <stdlib.h>
 #include <string.h>
 #include <complex.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 typedef struct { double re, im; } zc;
 
@@ -195,26 +198,49 @@ static double fro(const zc* M, size_t n) {
 static void gemm_core(fmt_t f, zc alpha, char opA, const zc* A, int lda, char opB,
                       const zc* B, int ldb, zc beta, const zc* C, int ldc,
                       zc* out, int ldo, int m, int n, int k) {
-  zc* acc = zalloc((size_t)m * n);
+  /* Parallel restatement: every output element accumulates its k products in
+   * ascending order starting from 0, exactly as the reference's rank-1 loop;
+   * only the order in which DIFFERENT elements are visited changes (row/column
+   * blocks per thread), so the result is bit-identical.  Operands are first
+   * copied into row-major op(A) (m x k) and op(B) (k x n); conjugation is exact. */
+  zc* Ao = zalloc((size_t)m * k);
+  zc* Bo = zalloc((size_t)k * n);
+#pragma omp parallel for schedule(static) if ((size_t)m * k > 4096)
+  for (int i = 0; i < m; i++)
+    for (int p = 0; p < k; p++) Ao[(size_t)i * k + p] = opA == 'N' ? AT(A, lda, i, p) : conjz(AT(A, lda, p, i));
+#pragma omp parallel for schedule(static) if ((size_t)n * k > 4096)
   for (int p = 0; p < k; p++)
-    for (int i = 0; i < m; i++) {
-      zc a = opA == 'N' ? AT(A, lda, i, p) : conjz(AT(A, lda, p, i));
-      for (int j = 0; j < n; j++) {
-        zc b = opB == 'N' ? AT(B, ldb, p, j) : conjz(AT(B, ldb, j, p));
-        acc[(size_t)i * n + j] = c_add(f, acc[(size_t)i * n + j], c_mul(f, a, b));
-      }
-    }
+    for (int j = 0; j < n; j++) Bo[(size_t)p * n + j] = opB == 'N' ? AT(B, ldb, p, j) : conjz(AT(B, ldb, j, p));
   int a1 = alpha.re == 1.0 && alpha.im == 0.0;
   int b0 = beta.re == 0.0 && beta.im == 0.0;
   int b1 = beta.re == 1.0 && beta.im == 0.0;
-  for (int i = 0; i < m; i++)
-    for (int j = 0; j < n; j++) {
-      zc v = acc[(size_t)i * n + j];
-      if (!a1) v = c_mul(f, alpha, v);
-      if (!b0) v = c_add(f, v, b1 ? AT(C, ldc, i, j) : c_mul(f, beta, AT(C, ldc, i, j)));
-      AT(out, ldo, i, j) = v;
+  enum { IB = 16, JB = 128 };
+  int nib = (m + IB - 1) / IB, njb = (n + JB - 1) / JB;
+#pragma omp parallel for collapse(2) schedule(dynamic) if ((double)m * n * k > 1e6)
+  for (int ib = 0; ib < nib; ib++)
+    for (int jb = 0; jb < njb; jb++) {
+      zc acc[IB][JB];
+      int i0 = ib * IB, i1 = i0 + IB < m ? i0 + IB : m;
+      int j0 = jb * JB, j1 = j0 + JB < n ? j0 + JB : n;
+      for (int i = i0; i < i1; i++)
+        for (int j = j0; j < j1; j++) acc[i - i0][j - j0] = Z(0.0, 0.0);
+      for (int p = 0; p < k; p++) {
+        const zc* brow = Bo + (size_t)p * n;
+        for (int i = i0; i < i1; i++) {
+          zc a = Ao[(size_t)i * k + p];
+          zc* ar = acc[i - i0];
+          for (int j = j0; j < j1; j++) ar[j - j0] = c_add(f, ar[j - j0], c_mul(f, a, brow[j]));
+        }
+      }
+      for (int i = i0; i < i1; i++)
+        for (int j = j0; j < j1; j++) {
+          zc v = acc[i - i0][j - j0];
+          if (!a1) v = c_mul(f, alpha, v);
+          if (!b0) v = c_add(f, v, b1 ? AT(C, ldc, i, j) : c_mul(f, beta, AT(C, ldc, i, j)));
+          AT(out, ldo, i, j) = v;
+        }
     }
-  free(acc);
+  free(Ao); free(Bo);
 }
 
 int oracle_gemm(int f32, double ar, double ai, const zc* A, const zc* B, double br,
@@ -260,30 +286,44 @@ static int make_reflector(fmt_t f, const zc* x, int n, int stride, zc* w, double
   return 1;
 }
 
-/* M[r0:r0+len, c0:c1] <- (I - beta w w*) M  (rows matching w) */
+/* M[r0:r0+len, c0:c1] <- (I - beta w w*) M  (rows matching w).
+ * Parallel over columns: each t[j] accumulates over i ascending, each M entry
+ * gets its single update -- the reference's per-element order. */
 static void refl_left(fmt_t f, zc* M, int ld, int r0, int c0, int c1, const zc* w, int len, double beta, zc* t) {
-  for (int j = c0; j < c1; j++) t[j - c0] = Z(0.0, 0.0);
-  for (int i = 0; i < len; i++) {
-    zc wc = conjz(w[i]);
-    for (int j = c0; j < c1; j++) t[j - c0] = c_add(f, t[j - c0], c_mul(f, wc, AT(M, ld, r0 + i, j)));
+  zc* bw = zalloc(len);
+  for (int i = 0; i < len; i++) bw[i] = c_mul(f, Z(beta, 0.0), w[i]);
+  enum { CB = 32 };
+  int nb = (c1 - c0 + CB - 1) / CB;
+#pragma omp parallel for schedule(static) if ((size_t)len * (c1 - c0) > 32768)
+  for (int b = 0; b < nb; b++) {
+    int j0 = c0 + b * CB, j1 = j0 + CB < c1 ? j0 + CB : c1;
+    for (int j = j0; j < j1; j++) t[j - c0] = Z(0.0, 0.0);
+    for (int i = 0; i < len; i++) {
+      zc wc = conjz(w[i]);
+      const zc* row = &AT(M, ld, r0 + i, 0);
+      for (int j = j0; j < j1; j++) t[j - c0] = c_add(f, t[j - c0], c_mul(f, wc, row[j]));
+    }
+    for (int i = 0; i < len; i++) {
+      zc* row = &AT(M, ld, r0 + i, 0);
+      for (int j = j0; j < j1; j++) row[j] = c_sub(f, row[j], c_mul(f, bw[i], t[j - c0]));
+    }
   }
-  for (int i = 0; i < len; i++) {
-    zc bw = c_mul(f, Z(beta, 0.0), w[i]);
-    for (int j = c0; j < c1; j++)
-      AT(M, ld, r0 + i, j) = c_sub(f, AT(M, ld, r0 + i, j), c_mul(f, bw, t[j - c0]));
-  }
+  free(bw);
 }
 
-/* M[r0:r1, c0:c0+len] <- M (I - beta w w*)  (columns matching w) */
+/* M[r0:r1, c0:c0+len] <- M (I - beta w w*)  (columns matching w); parallel over rows */
 static void refl_right(fmt_t f, zc* M, int ld, int r0, int r1, int c0, const zc* w, int len, double beta, zc* t) {
-  for (int r = r0; r < r1; r++) t[r - r0] = Z(0.0, 0.0);
-  for (int i = 0; i < len; i++)
-    for (int r = r0; r < r1; r++) t[r - r0] = c_add(f, t[r - r0], c_mul(f, AT(M, ld, r, c0 + i), w[i]));
-  for (int i = 0; i < len; i++) {
-    zc bw = c_mul(f, Z(beta, 0.0), conjz(w[i]));
-    for (int r = r0; r < r1; r++)
-      AT(M, ld, r, c0 + i) = c_sub(f, AT(M, ld, r, c0 + i), c_mul(f, t[r - r0], bw));
+  zc* bw = zalloc(len);
+  for (int i = 0; i < len; i++) bw[i] = c_mul(f, Z(beta, 0.0), conjz(w[i]));
+#pragma omp parallel for schedule(static) if ((size_t)len * (r1 - r0) > 32768)
+  for (int r = r0; r < r1; r++) {
+    zc* row = &AT(M, ld, r, c0);
+    zc s = Z(0.0, 0.0);
+    for (int i = 0; i < len; i++) s = c_add(f, s, c_mul(f, row[i], w[i]));
+    t[r - r0] = s;
+    for (int i = 0; i < len; i++) row[i] = c_sub(f, row[i], c_mul(f, s, bw[i]));
   }
+  free(bw);
 }
 
 /* ---------------------------------------------------------------------- */
@@ -336,24 +376,6 @@ static void givens(fmt_t f, zc fv, zc g, double* c, zc* s) {
   *s = c_div(f, c_mul(f, c_div(f, fv, Z(af, 0.0)), conjz(g)), Z(d, 0.0));
 }
 
-static void rot_rows(fmt_t f, zc* H, int ld, int k, double c, zc s, int j0, int j1) {
-  zc cc = Z(c, 0.0), sc = conjz(s);
-  for (int j = j0; j < j1; j++) {
-    zc r1 = AT(H, ld, k, j), r2 = AT(H, ld, k + 1, j);
-    AT(H, ld, k, j) = c_add(f, c_mul(f, cc, r1), c_mul(f, s, r2));
-    AT(H, ld, k + 1, j) = c_sub(f, c_mul(f, cc, r2), c_mul(f, sc, r1));
-  }
-}
-
-static void rot_cols(fmt_t f, zc* H, int ld, int k, double c, zc s, int i0, int i1) {
-  zc cc = Z(c, 0.0), sc = conjz(s);
-  for (int i = i0; i < i1; i++) {
-    zc c1 = AT(H, ld, i, k), c2 = AT(H, ld, i, k + 1);
-    AT(H, ld, i, k) = c_add(f, c_mul(f, cc, c1), c_mul(f, sc, c2));
-    AT(H, ld, i, k + 1) = c_sub(f, c_mul(f, cc, c2), c_mul(f, s, c1));
-  }
-}
-
 static zc wilkinson_shift(fmt_t f, const zc* H, int m, int hi) {
   zc a = AT(H, m, hi - 1, hi - 1), b = AT(H, m, hi - 1, hi);
   zc c = AT(H, m, hi, hi - 1), d = AT(H, m, hi, hi);
@@ -365,12 +387,45 @@ static zc wilkinson_shift(fmt_t f, const zc* H, int m, int hi) {
   return c_sub(f, d, c_div(f, c_mul(f, b, c), denom));
 }
 
+/* One QR sweep's rotations, applied in batches of SWEEP_BATCH chase steps.
+ *
+ * The reference (linalg.py:518-577) applies, at each step k of a sweep, the
+ * Givens rotation G_k to rows k, k+1 (columns max(lo,k-1)..m-1), then to
+ * columns k, k+1 of H (rows 0..min(k+3,hi+1)-1) and of U (all rows).  Each
+ * matrix entry therefore sees a fixed sequence of updates.  This restatement
+ * keeps that per-entry sequence exactly (so the result is bit-identical) but
+ * lets independent entries be updated by different threads:
+ *   phase A (sequential, the chase): steps K..K+S-1 on the columns < K+S+3
+ *     and the rows >= K-2 -- everything the next Givens rotations read;
+ *   phase B (parallel over columns >= K+S+3): the batch's row rotations, in
+ *     ascending k (those columns receive no column rotation in the batch);
+ *   phase C (parallel over rows, at the end of the sweep): the column
+ *     rotations deferred from rows < K-2 (which no later step reads) and all
+ *     rotations of U, each row in ascending k. */
+enum { SWEEP_BATCH = 32 };
+
+/* rows != 0: the rot_rows pair update; rows == 0: the rot_cols pair update */
+static inline void rot_pair(fmt_t f, zc* a, zc* b, double c, zc s, int rows) {
+  zc cc = Z(c, 0.0), sc = conjz(s);
+  zc v1 = *a, v2 = *b;
+  if (rows) {
+    *a = c_add(f, c_mul(f, cc, v1), c_mul(f, s, v2));
+    *b = c_sub(f, c_mul(f, cc, v2), c_mul(f, sc, v1));
+  } else {
+    *a = c_add(f, c_mul(f, cc, v1), c_mul(f, sc, v2));
+    *b = c_sub(f, c_mul(f, cc, v2), c_mul(f, s, v1));
+  }
+}
+
 /* schur: returns OR_ITERATION_LIMIT after 30*m sweeps; *sweeps_out optional */
 static int schur_core(fmt_t f, zc* H, zc* U, int m, int* sweeps_out) {
   if (m == 1) { U[0] = Z(1.0, 0.0); return OR_OK; }
   hessenberg(f, H, U, m);
   double u = f.f32 ? ldexp(1.0, -24) : ldexp(1.0, -53);
   int limit = 30 * m, sweeps = 0, stuck = 0, hi = m - 1;
+  double* cs = (double*)malloc(sizeof(double) * m);
+  zc* ss = zalloc(m);
+  int rc = OR_OK;
   while (hi > 0) {
     for (int k = 1; k <= hi; k++) {
       zc h = AT(H, m, k, k - 1);
@@ -381,7 +436,7 @@ static int schur_core(fmt_t f, zc* H, zc* U, int m, int* sweeps_out) {
     if (zero(AT(H, m, hi, hi - 1))) { hi--; stuck = 0; continue; }
     int lo = hi;
     while (lo > 0 && !zero(AT(H, m, lo, lo - 1))) lo--;
-    if (sweeps >= limit) { if (sweeps_out) *sweeps_out = sweeps; return OR_ITERATION_LIMIT; }
+    if (sweeps >= limit) { rc = OR_ITERATION_LIMIT; break; }
     zc shift;
     if (stuck > 0 && stuck % 10 == 0) {
       zc h1 = AT(H, m, hi, hi - 1), h2 = AT(H, m, hi, hi);
@@ -391,21 +446,57 @@ static int schur_core(fmt_t f, zc* H, zc* U, int m, int* sweeps_out) {
     }
     zc x = c_sub_exact(f, AT(H, m, lo, lo), shift);
     zc y = AT(H, m, lo + 1, lo);
-    for (int k = lo; k < hi; k++) {
-      double c; zc s;
-      givens(f, x, y, &c, &s);
-      int j0 = lo > k - 1 ? lo : k - 1;
-      rot_rows(f, H, m, k, c, s, j0, m);
-      rot_cols(f, H, m, k, c, s, 0, (k + 3 < hi + 1) ? k + 3 : hi + 1);
-      rot_cols(f, U, m, k, c, s, 0, m);
-      if (k > lo) AT(H, m, k + 1, k - 1) = Z(0.0, 0.0);
-      if (k < hi - 1) { x = AT(H, m, k + 1, k); y = AT(H, m, k + 2, k); }
+    for (int K = lo; K < hi; K += SWEEP_BATCH) {
+      int Ke = K + SWEEP_BATCH < hi ? K + SWEEP_BATCH : hi;
+      int cnear = Ke + 3 < m ? Ke + 3 : m;
+      int rfar = K - 2 > 0 ? K - 2 : 0;
+      /* phase A */
+      for (int k = K; k < Ke; k++) {
+        double c; zc s;
+        givens(f, x, y, &c, &s);
+        cs[k] = c; ss[k] = s;
+        int j0 = lo > k - 1 ? lo : k - 1;
+        for (int j = j0; j < cnear; j++) rot_pair(f, &AT(H, m, k, j), &AT(H, m, k + 1, j), c, s, 1);
+        int i1 = (k + 3 < hi + 1) ? k + 3 : hi + 1;
+        for (int i = rfar; i < i1; i++) rot_pair(f, &AT(H, m, i, k), &AT(H, m, i, k + 1), c, s, 0);
+        if (k > lo) AT(H, m, k + 1, k - 1) = Z(0.0, 0.0);
+        if (k < hi - 1) { x = AT(H, m, k + 1, k); y = AT(H, m, k + 2, k); }
+      }
+      /* phase B */
+      enum { CB = 8 };
+      int nb = (m - cnear + CB - 1) / CB;
+#pragma omp parallel for schedule(static) if (nb * (Ke - K) > 512)
+      for (int b = 0; b < nb; b++) {
+        int c0 = cnear + b * CB, c1 = c0 + CB < m ? c0 + CB : m;
+        for (int k = K; k < Ke; k++) {
+          zc* r0 = &AT(H, m, k, 0);
+          zc* r1 = &AT(H, m, k + 1, 0);
+          for (int j = c0; j < c1; j++) rot_pair(f, r0 + j, r1 + j, cs[k], ss[k], 1);
+        }
+      }
+    }
+    /* phase C: deferred column rotations of H (rows < K-2 of each batch) and all of U */
+#pragma omp parallel for schedule(static) if ((size_t)m * (hi - lo) > 16384)
+    for (int r = 0; r < 2 * m; r++) {
+      if (r < m) {
+        zc* row = &AT(H, m, r, 0);
+        for (int K = lo; K < hi; K += SWEEP_BATCH) {
+          if (!(r < K - 2)) continue;
+          int Ke = K + SWEEP_BATCH < hi ? K + SWEEP_BATCH : hi;
+          for (int k = K; k < Ke; k++) rot_pair(f, row + k, row + k + 1, cs[k], ss[k], 0);
+        }
+      } else {
+        zc* row = &AT(U, m, r - m, 0);
+        for (int k = lo; k < hi; k++) rot_pair(f, row + k, row + k + 1, cs[k], ss[k], 0);
+      }
     }
     sweeps++; stuck++;
   }
+  free(cs); free(ss);
+  if (sweeps_out) *sweeps_out = sweeps;
+  if (rc) return rc;
   for (int i = 0; i < m; i++)
     for (int j = 0; j < i; j++) AT(H, m, i, j) = Z(0.0, 0.0);
-  if (sweeps_out) *sweeps_out = sweeps;
   return OR_OK;
 }
 
@@ -420,33 +511,43 @@ int oracle_schur(int f32, const zc* A, zc* T, zc* U, int m, int* sweeps) {
 /* MGS QR with positive diagonal (linalg.py:228-273), binary64 or binary32  */
 
 static int mgs_qr_core(fmt_t f, const zc* A_in, zc* Q, zc* R, int m, int n) {
+  /* Right-looking restatement: once q_i is final, every later column j
+   * projects against it (in parallel over j).  Column j still sees the
+   * projections i = 0, 1, ..., j-1 in that order with the reference's
+   * arithmetic, so Q and R are bit-identical to the column-by-column loop. */
   int rc = enter(f, A_in, Q, (size_t)m * n);
   if (rc) return rc;
   double nrmA = fro(Q, (size_t)m * n);
   memset(R, 0, sizeof(zc) * (size_t)n * n);
-  zc* v = zalloc(m);
-  for (int j = 0; j < n; j++) {
-    for (int i = 0; i < m; i++) v[i] = AT(Q, n, i, j);
-    for (int i = 0; i < j; i++) {
+  zc* V = zalloc((size_t)n * m); /* row j = column j */
+  for (int i = 0; i < m; i++)
+    for (int j = 0; j < n; j++) V[(size_t)j * m + i] = AT(Q, n, i, j);
+  for (int i = 0; i < n; i++) {
+    zc* q = V + (size_t)i * m;
+    double nv = vec_norm2(f, q, m, 1);
+    AT(R, n, i, i) = Z(nv, 0.0);
+    if (nv == 0.0) { free(V); return OR_RANK_DEFICIENT; }
+    for (int p = 0; p < m; p++) q[p] = c_div(f, q[p], Z(nv, 0.0));
+#pragma omp parallel for schedule(static) if ((size_t)(n - i - 1) * m > 16384)
+    for (int j = i + 1; j < n; j++) {
+      zc* v = V + (size_t)j * m;
       zc r = Z(0.0, 0.0);
       if (!f.f32) {
         for (int p = 0; p < m; p++) {
-          zc q = AT(Q, n, p, i);
-          r.re += q.re * v[p].re + q.im * v[p].im;
-          r.im += q.re * v[p].im - q.im * v[p].re;
+          zc qq = q[p];
+          r.re += qq.re * v[p].re + qq.im * v[p].im;
+          r.im += qq.re * v[p].im - qq.im * v[p].re;
         }
       } else {
-        for (int p = 0; p < m; p++) r = c_add(f, r, c_mul(f, conjz(AT(Q, n, p, i)), v[p]));
+        for (int p = 0; p < m; p++) r = c_add(f, r, c_mul(f, conjz(q[p]), v[p]));
       }
       AT(R, n, i, j) = r;
-      for (int p = 0; p < m; p++) v[p] = c_sub(f, v[p], c_mul(f, r, AT(Q, n, p, i)));
+      for (int p = 0; p < m; p++) v[p] = c_sub(f, v[p], c_mul(f, r, q[p]));
     }
-    double nv = vec_norm2(f, v, m, 1);
-    AT(R, n, j, j) = Z(nv, 0.0);
-    if (nv == 0.0) { free(v); return OR_RANK_DEFICIENT; }
-    for (int p = 0; p < m; p++) AT(Q, n, p, j) = c_div(f, v[p], Z(nv, 0.0));
   }
-  free(v);
+  for (int i = 0; i < m; i++)
+    for (int j = 0; j < n; j++) AT(Q, n, i, j) = V[(size_t)j * m + i];
+  free(V);
   /* _fix_r_diagonal: R[j,j] = nv is real positive already (phase == 1) */
   double u = f.f32 ? ldexp(1.0, -24) : ldexp(1.0, -53);
   double dmin = INFINITY;
@@ -477,9 +578,11 @@ static int lu_core(fmt_t f, const zc* A_in, zc* W, long long* piv, int n) {
     if (p != k)
       for (int j = 0; j < n; j++) { zc tmp = AT(W, n, k, j); AT(W, n, k, j) = AT(W, n, p, j); AT(W, n, p, j) = tmp; }
     for (int i = k + 1; i < n; i++) AT(W, n, i, k) = c_div(f, AT(W, n, i, k), AT(W, n, k, k));
-    for (int i = k + 1; i < n; i++)
-      for (int j = k + 1; j < n; j++)
-        AT(W, n, i, j) = c_sub(f, AT(W, n, i, j), c_mul(f, AT(W, n, i, k), AT(W, n, k, j)));
+#pragma omp parallel for schedule(static) if ((size_t)(n - k) * (n - k) > 16384)
+    for (int i = k + 1; i < n; i++) {
+      zc l = AT(W, n, i, k);
+      for (int j = k + 1; j < n; j++) AT(W, n, i, j) = c_sub(f, AT(W, n, i, j), c_mul(f, l, AT(W, n, k, j)));
+    }
   }
   return OR_OK;
 }
@@ -498,37 +601,56 @@ static void apply_pivots(zc* B, int nrhs, const long long* piv, int n, int inver
   }
 }
 
-/* _solve_lower / _solve_upper on X (n x nrhs) in place */
-static int solve_lower(fmt_t f, const zc* L, int n, zc* X, int nrhs, int unit, int cj) {
-  for (int i = 0; i < n; i++) {
-    if (!unit) {
-      zc d = cj ? conjz(AT(L, n, i, i)) : AT(L, n, i, i);
-      if (zero(d)) return OR_SINGULAR_MATRIX;
-      for (int j = 0; j < nrhs; j++) AT(X, nrhs, i, j) = c_div(f, AT(X, nrhs, i, j), d);
+/* _solve_lower / _solve_upper on X (n x nrhs) in place.  Restated in row
+ * (dot-product) order: row r receives the updates from rows i = 0..r-1
+ * (lower) or i = n-1..r+1 (upper) in the same order as the reference's
+ * column sweep, then its diagonal division -- identical per-entry arithmetic.
+ * Right-hand-side columns are independent and split across threads. */
+static int solve_tri(fmt_t f, const zc* L, int n, zc* X, int nrhs, int unit, int cj, int upper) {
+  if (!unit)
+    for (int t = 0; t < n; t++) {
+      int i = upper ? n - 1 - t : t;
+      if (zero(AT(L, n, i, i))) return OR_SINGULAR_MATRIX;
     }
-    for (int r = i + 1; r < n; r++) {
-      zc col = cj ? conjz(AT(L, n, i, r)) : AT(L, n, r, i);
-      for (int j = 0; j < nrhs; j++)
-        AT(X, nrhs, r, j) = c_sub(f, AT(X, nrhs, r, j), c_mul(f, col, AT(X, nrhs, i, j)));
+  /* op(L)[r][i] row-contiguous */
+  zc* Lo = zalloc((size_t)n * n);
+#pragma omp parallel for schedule(static) if ((size_t)n * n > 16384)
+  for (int r = 0; r < n; r++)
+    for (int i = 0; i < n; i++) Lo[(size_t)r * n + i] = cj ? conjz(AT(L, n, i, r)) : AT(L, n, r, i);
+  enum { JC = 16 };
+  int nch = (nrhs + JC - 1) / JC;
+#pragma omp parallel for schedule(dynamic) if ((size_t)n * n * nrhs > 100000)
+  for (int c = 0; c < nch; c++) {
+    int j0 = c * JC, j1 = j0 + JC < nrhs ? j0 + JC : nrhs;
+    for (int t = 0; t < n; t++) {
+      int r = upper ? n - 1 - t : t;
+      zc* xr = &AT(X, nrhs, r, 0);
+      const zc* lr = Lo + (size_t)r * n;
+      if (!upper) {
+        for (int i = 0; i < r; i++) {
+          const zc* xi = &AT(X, nrhs, i, 0);
+          for (int j = j0; j < j1; j++) xr[j] = c_sub(f, xr[j], c_mul(f, lr[i], xi[j]));
+        }
+      } else {
+        for (int i = n - 1; i > r; i--) {
+          const zc* xi = &AT(X, nrhs, i, 0);
+          for (int j = j0; j < j1; j++) xr[j] = c_sub(f, xr[j], c_mul(f, lr[i], xi[j]));
+        }
+      }
+      if (!unit) {
+        zc d = lr[r];
+        for (int j = j0; j < j1; j++) xr[j] = c_div(f, xr[j], d);
+      }
     }
   }
+  free(Lo);
   return OR_OK;
 }
-
+static int solve_lower(fmt_t f, const zc* L, int n, zc* X, int nrhs, int unit, int cj) {
+  return solve_tri(f, L, n, X, nrhs, unit, cj, 0);
+}
 static int solve_upper(fmt_t f, const zc* Um, int n, zc* X, int nrhs, int unit, int cj) {
-  for (int i = n - 1; i >= 0; i--) {
-    if (!unit) {
-      zc d = cj ? conjz(AT(Um, n, i, i)) : AT(Um, n, i, i);
-      if (zero(d)) return OR_SINGULAR_MATRIX;
-      for (int j = 0; j < nrhs; j++) AT(X, nrhs, i, j) = c_div(f, AT(X, nrhs, i, j), d);
-    }
-    for (int r = 0; r < i; r++) {
-      zc col = cj ? conjz(AT(Um, n, i, r)) : AT(Um, n, r, i);
-      for (int j = 0; j < nrhs; j++)
-        AT(X, nrhs, r, j) = c_sub(f, AT(X, nrhs, r, j), c_mul(f, col, AT(X, nrhs, i, j)));
-    }
-  }
-  return OR_OK;
+  return solve_tri(f, Um, n, X, nrhs, unit, cj, 1);
 }
 
 /* lu_solve(F, B, side, transpose); left: B is n x nrhs; right: B is nrows x n */
@@ -580,6 +702,11 @@ static int is_lower(const zc* T, int n) {
 }
 
 static int solve_sylv_tri_core(fmt_t f, const zc* TA, int m, const zc* TB, int n, const zc* C, zc* Y) {
+  /* Column recurrence of sylvester.py:111-157.  Restated with (i) the back
+   * substitution blocked by row panels -- row r still receives its updates
+   * from i = m-1 down to r+1 in that order -- and the updates of the rows
+   * above a panel split across threads, (ii) the rank-1 update of the
+   * remaining columns split by rows.  Per-entry arithmetic is unchanged. */
   if (!(m == 1 || is_upper(TA, m))) return OR_DIMENSION;
   int lower = 0;
   if (n > 1 && !is_upper(TB, n)) {
@@ -590,28 +717,39 @@ static int solve_sylv_tri_core(fmt_t f, const zc* TA, int m, const zc* TB, int n
   zc* col = zalloc(m);
   zc* y = zalloc(m);
   int rc = OR_OK;
+  enum { PB = 128 };
   for (int t = 0; t < n && !rc; t++) {
     int j = lower ? n - 1 - t : t;
     zc shift = AT(TB, n, j, j);
     for (int i = 0; i < m; i++) { col[i] = AT(W, n, i, j); y[i] = Z(0.0, 0.0); }
-    for (int i = m - 1; i >= 0; i--) {
-      zc d = c_add(f, AT(TA, m, i, i), shift);
-      if (zero(d)) { g_err_row = i; g_err_col = j; rc = OR_SINGULAR_EQUATION; break; }
-      y[i] = c_div(f, col[i], d);
-      for (int r = 0; r < i; r++) col[r] = c_sub(f, col[r], c_mul(f, AT(TA, m, r, i), y[i]));
+    for (int r1 = m; r1 > 0 && !rc; r1 -= PB) {
+      int r0 = r1 - PB > 0 ? r1 - PB : 0;
+      for (int i = r1 - 1; i >= r0; i--) {
+        zc d = c_add(f, AT(TA, m, i, i), shift);
+        if (zero(d)) { g_err_row = i; g_err_col = j; rc = OR_SINGULAR_EQUATION; break; }
+        y[i] = c_div(f, col[i], d);
+        for (int r = r0; r < i; r++) col[r] = c_sub(f, col[r], c_mul(f, AT(TA, m, r, i), y[i]));
+      }
+      if (rc) break;
+#pragma omp parallel for schedule(static) if ((size_t)r0 * (r1 - r0) > 32768)
+      for (int r = 0; r < r0; r++) {
+        const zc* tr = &AT(TA, m, r, 0);
+        zc v = col[r];
+        for (int i = r1 - 1; i >= r0; i--) v = c_sub(f, v, c_mul(f, tr[i], y[i]));
+        col[r] = v;
+      }
     }
     if (rc) break;
     for (int i = 0; i < m; i++) if (!zfinite(y[i])) { rc = OR_NUMERIC_BREAKDOWN; g_err_col = j; break; }
     if (rc) break;
     for (int i = 0; i < m; i++) AT(Y, n, i, j) = y[i];
-    if (!lower) {
-      for (int i = 0; i < m; i++)
-        for (int jj = j + 1; jj < n; jj++)
-          AT(W, n, i, jj) = c_sub(f, AT(W, n, i, jj), c_mul(f, y[i], AT(TB, n, j, jj)));
-    } else {
-      for (int i = 0; i < m; i++)
-        for (int jj = 0; jj < j; jj++)
-          AT(W, n, i, jj) = c_sub(f, AT(W, n, i, jj), c_mul(f, y[i], AT(TB, n, j, jj)));
+    int c0 = lower ? 0 : j + 1, c1 = lower ? j : n;
+#pragma omp parallel for schedule(static) if ((size_t)m * (c1 - c0) > 32768)
+    for (int i = 0; i < m; i++) {
+      zc yi = y[i];
+      zc* wr = &AT(W, n, i, 0);
+      const zc* tb = &AT(TB, n, j, 0);
+      for (int jj = c0; jj < c1; jj++) wr[jj] = c_sub(f, wr[jj], c_mul(f, yi, tb[jj]));
     }
   }
   free(W); free(col); free(y);
@@ -632,25 +770,34 @@ int oracle_solve_sylv_tri(int f32, const zc* TA, int m, const zc* TB, int n, con
 /* residual metric (sylvester.py:199-209), binary64                         */
 
 double oracle_residual(const zc* A, const zc* B, const zc* C, const zc* X, int m, int n) {
+  /* ||A X + X B - C||_F / (||C||_F + ||X||_F (||A||_F + ||B||_F)) in binary64.
+   * The reference evaluates the products with numpy/OpenBLAS, so only the
+   * value (to a few ulps), not the summation order, is restated. */
+  fmt_t fh = {0};
+  zc* AX = zalloc((size_t)m * n);
+  zc* XB = zalloc((size_t)m * n);
+  gemm_core(fh, Z(1.0, 0.0), 'N', A, m, 'N', X, n, Z(0.0, 0.0), NULL, 0, AX, n, m, n, m);
+  gemm_core(fh, Z(1.0, 0.0), 'N', X, n, 'N', B, n, Z(0.0, 0.0), NULL, 0, XB, n, m, n, n);
   double num = 0.0;
-  for (int i = 0; i < m; i++)
-    for (int j = 0; j < n; j++) {
-      double sr = 0.0, si = 0.0;
-      for (int p = 0; p < m; p++) {
-        zc a = AT(A, m, i, p), x = AT(X, n, p, j);
-        sr += a.re * x.re - a.im * x.im; si += a.re * x.im + a.im * x.re;
-      }
-      for (int p = 0; p < n; p++) {
-        zc x = AT(X, n, i, p), b = AT(B, n, p, j);
-        sr += x.re * b.re - x.im * b.im; si += x.re * b.im + x.im * b.re;
-      }
-      sr -= AT(C, n, i, j).re; si -= AT(C, n, i, j).im;
-      num += sr * sr + si * si;
-    }
+  for (size_t e = 0; e < (size_t)m * n; e++) {
+    double sr = AX[e].re + XB[e].re - C[e].re, si = AX[e].im + XB[e].im - C[e].im;
+    num += sr * sr + si * si;
+  }
+  free(AX); free(XB);
   num = sqrt(num);
   double den = fro(C, (size_t)m * n) + fro(X, (size_t)m * n) * (fro(A, (size_t)m * m) + fro(B, (size_t)n * n));
   if (den == 0.0) return 0.0;
   return num / den;
+}
+
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
 }
 
 /* ---------------------------------------------------------------------- */

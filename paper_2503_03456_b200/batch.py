@@ -19,6 +19,14 @@ from . import device as D
 from .errors import DeviceError, DimensionError
 
 
+DEFAULT_LANES = 64  # kDefaultLanes in csrc/solver.cu
+
+
+def effective_lanes(lanes: int, batch: int) -> int:
+    """Lanes the executor actually runs: min(lanes or the default, batch), at least 1."""
+    return max(1, min(lanes if lanes > 0 else DEFAULT_LANES, batch))
+
+
 def _params(m, n, cx, kind, variant, low_bits, correction_bits, epsilon, max_iter, y0_zero):
     p = _native.Params()
     p.m, p.n = m, n
@@ -60,7 +68,8 @@ def solve_batched(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, *, kind: st
     p = _params(n, m, cx, kind, variant, low_bits, correction_bits, eps, max_iter, y0_zero)
     L = _native.lib()
     sz = ct.c_size_t()
-    _native.check(L.sylv_batched_workspace_size(ct.byref(p), int(lanes), ct.byref(sz)), "workspace query")
+    lanes = effective_lanes(int(lanes), nb)
+    _native.check(L.sylv_batched_workspace_size(ct.byref(p), lanes, ct.byref(sz)), "workspace query")
     ws = D.workspace(sz.value, A.device)
     Arr = ct.c_void_p * nb
     es = A.element_size()

@@ -199,34 +199,48 @@ inline bool& host_sync_blocking() {
   thread_local bool b = false;
   return b;
 }
+// Per-thread resources of the host waits, released when the thread exits (the solve path
+// may run on short-lived threads, e.g. the batched executor's lane workers).
+struct ThreadSyncEvent {
+  cudaEvent_t ev = nullptr;
+  ~ThreadSyncEvent() {
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+struct ThreadPinnedStage {
+  void* p = nullptr;
+  ~ThreadPinnedStage() {
+    if (p) cudaFreeHost(p);
+  }
+};
 inline cudaError_t host_sync(cudaStream_t st) {
   if (!host_sync_blocking()) return cudaStreamSynchronize(st);
-  thread_local cudaEvent_t ev = nullptr;
-  if (!ev) {
-    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventBlockingSync | cudaEventDisableTiming);
-    if (e != cudaSuccess) return e;
+  thread_local ThreadSyncEvent tev;
+  if (!tev.ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&tev.ev, cudaEventBlockingSync | cudaEventDisableTiming);
+    if (e != cudaSuccess) { tev.ev = nullptr; return e; }
   }
-  cudaError_t e = cudaEventRecord(ev, st);
+  cudaError_t e = cudaEventRecord(tev.ev, st);
   if (e != cudaSuccess) return e;
-  return cudaEventSynchronize(ev);
+  return cudaEventSynchronize(tev.ev);
 }
 
 // Small device -> host readbacks (status words, norms) go through a per-thread
 // pinned staging buffer: a copy into pageable memory would make the driver stage
 // it synchronously, which serialises concurrent solve lanes.
 inline cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-  thread_local void* pinned = nullptr;
+  thread_local ThreadPinnedStage stage;
   constexpr size_t kCap = 4096;
   if (bytes > kCap) return cudaErrorInvalidValue;
-  if (!pinned) {
-    cudaError_t e = cudaHostAlloc(&pinned, kCap, cudaHostAllocPortable);
-    if (e != cudaSuccess) { pinned = nullptr; return e; }
+  if (!stage.p) {
+    cudaError_t e = cudaHostAlloc(&stage.p, kCap, cudaHostAllocPortable);
+    if (e != cudaSuccess) { stage.p = nullptr; return e; }
   }
-  cudaError_t e = cudaMemcpyAsync(pinned, src, bytes, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaMemcpyAsync(stage.p, src, bytes, cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return e;
   e = host_sync(st);
   if (e != cudaSuccess) return e;
-  memcpy(dst, pinned, bytes);
+  memcpy(dst, stage.p, bytes);
   return cudaSuccess;
 }
 

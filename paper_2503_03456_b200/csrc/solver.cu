@@ -168,8 +168,27 @@ int read_trsyl_status(int* dstat, int m, int n, int lowerB, int* row, int* col, 
   return SYLV_SINGULAR_EQUATION;
 }
 
+// Column index (0-based, in the matrix) of the first column in solve order holding a
+// non-finite entry; -1 if none.  Only called on the failure path.
+template <class S>
+int first_nonfinite_col(const S* X, int rows, int cols, int ld, int lowerB, int* dint, int* col, cudaStream_t st) {
+  first_nonfinite_init_kernel<<<1, 1, 0, st>>>(dint);
+  MSY_LAUNCH_CK();
+  long tot = (long)rows * cols;
+  int nb = (int)std::min<long>(RED_BLOCKS, std::max<long>(1, cdiv(tot, RED_TPB)));
+  first_nonfinite_kernel<S><<<nb, RED_TPB, 0, st>>>(rows, cols, X, ld, lowerB, dint);
+  MSY_LAUNCH_CK();
+  int h = 0;
+  MSY_CK(d2h(&h, dint, sizeof(int), st));
+  *col = h == 0x7fffffff ? -1 : (lowerB ? cols - 1 - h : h);
+  return 0;
+}
+
 // The refinement loop (Alg. 1, refinement.py:95-141) on device buffers:
 // S_A = T_A + dT_A and S_B = T_B + dT_B already formed; T's in Hh.
+// One host readback per iteration: the trsyl status word, ||D||_F^2 and ||Y+D||_F^2 are
+// packed on the device (pack_status_kernel); the iterate update is guarded on the device
+// so a failed correction leaves Y as the reference leaves it.
 template <class Hh, class Ll>
 int refine_loop(int m, int n, const Hh* TAh, const Hh* TBh, int lowerB, const Hh* SA, const Hh* SB, const Hh* F, Hh* Y,
                 Hh* R, Ll* Rl, const Ll* TAl, const Ll* TBl, int corr_bits, double eps, int max_iter,
@@ -178,6 +197,9 @@ int refine_loop(int m, int n, const Hh* TAh, const Hh* TBh, int lowerB, const Hh
   rep->iterations = 0;
   rep->converged = 0;
   rep->n_norms = 0;
+  double* red_d = red;      // sumsq(D)
+  double* red_u = red + 3;  // guarded Y += D: sumsq(D), sumsq(Y), nonfinite
+  double* packed = red + 10;
   int i = 0;
   while (i < max_iter) {
     // R = F - S_A Y - Y S_B
@@ -188,6 +210,7 @@ int refine_loop(int m, int n, const Hh* TAh, const Hh* TBh, int lowerB, const Hh
     rc = gemm<Hh>('N', 'N', m, n, n, Hh(-1), Y, m, SB, n, Hh(1), R, m, st);
     if (rc) return rc;
     trsyl_status_init<<<1, 1, 0, st>>>(ints);
+    MSY_LAUNCH_CK();
     if (corr_bits == 32 && Rl != nullptr) {
       rc = convert<Ll, Hh>(m, n, R, m, Rl, m, nullptr, st);
       if (rc) return rc;
@@ -198,28 +221,31 @@ int refine_loop(int m, int n, const Hh* TAh, const Hh* TBh, int lowerB, const Hh
       rc = trsyl<Hh>(m, n, TAh, m, TBh, n, lowerB, R, m, tsh, ints, st);
     }
     if (rc) return rc;
-    int row = -1, col = -1;
-    int ts = read_trsyl_status(ints, m, n, lowerB, &row, &col, st);
-    if (ts < 0) return ts;
-    if (ts == SYLV_SINGULAR_EQUATION) {
+    rc = reduce<Hh>(0, m, n, R, m, nullptr, 0, part, red_d, st);
+    if (!rc) rc = reduce<Hh>(2, m, n, Y, m, R, m, part, red_u, st, red_d, ints);  // Y += D (guarded)
+    if (rc) return rc;
+    pack_status_kernel<<<1, 1, 0, st>>>(ints, red_d, red_u, packed);
+    MSY_LAUNCH_CK();
+    double o[5];
+    MSY_CK(d2h(o, packed, sizeof(o), st));
+    if ((int)o[0] != 0x7fffffff) {  // singular diagonal pair (refinement.py:242-245)
+      int hs = (int)o[0];
+      int crank = hs / m;
       rep->status = SYLV_SINGULAR_EQUATION;
       rep->fail_stage = SYLV_STAGE_REFINEMENT;
-      rep->fail_row = row;
-      rep->fail_col = col;
+      rep->fail_row = m - 1 - hs % m;
+      rep->fail_col = lowerB ? n - 1 - crank : crank;
       return 0;
     }
-    double o[3];
-    rc = read_reduce<Hh>(R, m, n, m, nullptr, 0, 0, part, red, o, st);
-    if (rc) return rc;
-    if (!std::isfinite(o[0])) {  // NumericBreakdownError inside solve_sylv_tri (refinement.py:125-127)
+    if (!std::isfinite(o[1])) {  // NumericBreakdownError inside solve_sylv_tri (refinement.py:125-127)
       rep->status = SYLV_NUMERIC_BREAKDOWN;
       rep->fail_stage = SYLV_STAGE_REFINEMENT;
+      rc = first_nonfinite_col<Hh>(R, m, n, m, lowerB, ints + 8, &rep->fail_col, st);
+      if (rc) return rc;
       break;
     }
-    rc = read_reduce<Hh>(Y, m, n, m, R, m, 2, part, red, o, st);  // Y += D
-    if (rc) return rc;
     i++;
-    double nD = std::sqrt(o[0]), nY = std::sqrt(o[1]);
+    double nD = std::sqrt(o[2]), nY = std::sqrt(o[3]);
     if (rep->n_norms < SYLV_MAX_NORMS) rep->correction_norms[rep->n_norms++] = nD;
     if (!(std::isfinite(nD) && std::isfinite(nY))) {  // refinement.py:133-135
       rep->status = SYLV_NUMERIC_BREAKDOWN;
@@ -234,6 +260,54 @@ int refine_loop(int m, int n, const Hh* TAh, const Hh* TBh, int lowerB, const Hh
   rep->iterations = i;
   if (rep->status == SYLV_OK && !rep->converged) rep->status = SYLV_NON_CONVERGENCE;
   return 0;
+}
+
+// One persistent host thread drives Schur(B) (and orth(B)/S_B) beside the calling thread's
+// Schur(A).  It replaces a std::thread per solve: its thread-local pinned staging buffer and
+// sync event are allocated once for the process.  Pair solves are serialised by pair_mutex()
+// (the side streams of g_ctx are shared).
+struct SideWorker {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::function<void()>* job = nullptr;
+  bool done = true;
+  SideWorker() {
+    std::thread([this]() {
+      for (;;) {
+        std::function<void()>* j;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [this] { return job != nullptr; });
+          j = job;
+        }
+        (*j)();
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          job = nullptr;
+          done = true;
+        }
+        cv.notify_all();
+      }
+    }).detach();
+  }
+  void start(std::function<void()>* j) {
+    std::lock_guard<std::mutex> lk(mu);
+    job = j;
+    done = false;
+    cv.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return done; });
+  }
+};
+inline SideWorker& side_worker() {
+  static SideWorker* w = new SideWorker();  // process lifetime (never joined)
+  return *w;
+}
+inline std::mutex& pair_mutex() {
+  static std::mutex m;
+  return m;
 }
 
 template <class Hh, class Ll>
@@ -258,6 +332,7 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
     if (!rc) rc = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, st, sb, sca);
     return rc;
   }
+  std::lock_guard<std::mutex> pair_lock(pair_mutex());
   MSY_CK(cudaEventRecord(g_ctx.ev_in, st));
   MSY_CK(cudaStreamWaitEvent(g_ctx.side, g_ctx.ev_in, 0));
   int dev;
@@ -274,18 +349,19 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
     explicit CapGuard(int c) : old(hess_grid_cap()) { hess_grid_cap() = c; }
     ~CapGuard() { hess_grid_cap() = old; }
   } cap_a(nsm / 2);
-  std::thread tb([&]() {
+  std::function<void()> job_b = [&]() {
     cudaSetDevice(dev);
     host_sync_blocking() = blocking;
     hess_grid_cap() = nsm / 2;
     rcb = convert<Ll, Hh>(n, n, B, ldb, w.TB, n, ovf_b, side);
     if (!rcb) rcb = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, side, sb, scb);
     if (!rcb && post_b && sb->status == 0) rcb = (*post_b)(side);
-  });
+  };
+  side_worker().start(&job_b);
   cudaStream_t sa_st = g_ctx.hiA;  // ev_in (recorded above, after convert(A)) orders it after st
-  MSY_CK(cudaStreamWaitEvent(sa_st, g_ctx.ev_in, 0));
-  rc = schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, sa_st, sa, &g_ctx.swA);
-  tb.join();
+  cudaError_t we = cudaStreamWaitEvent(sa_st, g_ctx.ev_in, 0);
+  rc = we == cudaSuccess ? schur_device<Ll>(m, w.TA, m, w.UA, m, w.swA, sa_st, sa, &g_ctx.swA) : SYLV_ECUDA;
+  side_worker().wait();  // always joined before job_b's captures go out of scope
   if (rc) return rc;
   if (rcb) return rcb;
   MSY_CK(cudaEventRecord(g_ctx.ev_a, sa_st));
@@ -467,7 +543,11 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
   if (ts == SYLV_OK) {
     rc = read_reduce<Ll>(w.Fl, m, n, m, nullptr, 0, 0, w.part, w.red, o, st);
     if (rc) return rc;
-    if (!std::isfinite(o[0])) ts = SYLV_NUMERIC_BREAKDOWN;
+    if (!std::isfinite(o[0])) {
+      ts = SYLV_NUMERIC_BREAKDOWN;
+      rc = first_nonfinite_col<Ll>(w.Fl, m, n, m, lyap ? 1 : 0, tstat + 8, &col, st);
+      if (rc) return rc;
+    }
   }
   if (ts != SYLV_OK) {
     if (!p->y0_zero) {
@@ -602,7 +682,11 @@ int bs_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb, co
     double o[3];
     rc = read_reduce<Hh>(w.F, m, n, m, nullptr, 0, 0, w.part, w.red, o, st);
     if (rc) return rc;
-    if (!std::isfinite(o[0])) ts = SYLV_NUMERIC_BREAKDOWN;
+    if (!std::isfinite(o[0])) {
+      ts = SYLV_NUMERIC_BREAKDOWN;
+      rc = first_nonfinite_col<Hh>(w.F, m, n, m, lyap ? 1 : 0, tstat + 8, &col, st);
+      if (rc) return rc;
+    }
   }
   if (ts != SYLV_OK) {
     rep->status = ts;
@@ -1033,7 +1117,11 @@ static int trsyl_entry(int m, int n, const void* TA, int ldta, const void* TB, i
     double o[3];
     rc = read_reduce<S>((S*)W, m, n, ldw, nullptr, 0, 0, part, part + 3 * RED_BLOCKS, o, st);
     if (rc) return rc;
-    if (!std::isfinite(o[0])) ts = SYLV_NUMERIC_BREAKDOWN;
+    if (!std::isfinite(o[0])) {
+      ts = SYLV_NUMERIC_BREAKDOWN;
+      rc = first_nonfinite_col<S>((S*)W, m, n, ldw, lowerB, stat + 4, &col, st);
+      if (rc) return rc;
+    }
   }
   if (info) { info[0] = ts; info[1] = row; info[2] = col; }
   return 0;

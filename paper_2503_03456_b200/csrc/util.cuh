@@ -93,12 +93,17 @@ __global__ void add_kernel(int rows, int cols, S* A, int lda, const S* __restric
 
 // partial sums over a grid-stride loop: out[b*3 + {0,1,2}]
 //   mode 0: sumsq(X);   mode 1: sumsq(X - Yv);   mode 2 (refine): Y += D, sumsq(D), sumsq(Y), nonfinite
+// guard (mode 2, optional): skip the update (all-zero partials) unless guard[0] -- the
+// previous pass's sumsq(D) -- is finite and the trsyl status word says OK, so a failed
+// correction leaves Y untouched as in refinement.py:123-127 (no host round trip needed).
 template <class S>
 __global__ void __launch_bounds__(RED_TPB) reduce_kernel(int mode, int rows, int cols, S* X, int ldx, const S* Yv,
-                                                         int ldy, double* part) {
+                                                         int ldy, double* part, const double* guard = nullptr,
+                                                         const int* tstat = nullptr) {
   __shared__ double buf[RED_TPB / 32];
   double a = 0, b = 0, c = 0;
-  const size_t tot = (size_t)rows * cols;
+  size_t tot = (size_t)rows * cols;
+  if (guard && (!isfinite(guard[0]) || (tstat && tstat[0] != 0x7fffffff))) tot = 0;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
     int i = (int)(e % rows), j = (int)(e / rows);
     if (mode == 0) {
@@ -135,14 +140,38 @@ __global__ void reduce_final_kernel(int nparts, const double* part, double* out)
 // out[0..2] = sums (sumsq, sumsq2, nonfinite count)
 template <class S>
 static int reduce(int mode, int rows, int cols, S* X, int ldx, const S* Yv, int ldy, double* part, double* out,
-                  cudaStream_t st) {
+                  cudaStream_t st, const double* guard = nullptr, const int* tstat = nullptr) {
   long tot = (long)rows * cols;
   int nb = (int)std::min<long>(RED_BLOCKS, std::max<long>(1, cdiv(tot, RED_TPB)));
-  reduce_kernel<S><<<nb, RED_TPB, 0, st>>>(mode, rows, cols, X, ldx, Yv, ldy, part);
+  reduce_kernel<S><<<nb, RED_TPB, 0, st>>>(mode, rows, cols, X, ldx, Yv, ldy, part, guard, tstat);
   MSY_LAUNCH_CK();
   reduce_final_kernel<<<1, RED_TPB, 0, st>>>(nb, part, out);
   MSY_LAUNCH_CK();
   return 0;
+}
+
+// The refinement loop's per-iteration status record, gathered on the device so the host
+// reads it with ONE copy: {trsyl status word, sumsq(D), sumsq(D) (guarded pass),
+// sumsq(Y + D), nonfinite count}.
+__global__ void pack_status_kernel(const int* tstat, const double* red_d, const double* red_u, double* out) {
+  out[0] = (double)tstat[0];
+  out[1] = red_d[0];
+  out[2] = red_u[0];
+  out[3] = red_u[1];
+  out[4] = red_u[2];
+}
+
+// First column (in the recurrence's solve order: ascending for an upper T_B, descending for
+// a lower one) holding a non-finite entry -- the column sylvester.py:147-149 names in its
+// NumericBreakdownError.  out[0] must start at INT_MAX (first_nonfinite_init_kernel).
+__global__ void first_nonfinite_init_kernel(int* out) { out[0] = 0x7fffffff; }
+template <class S>
+__global__ void first_nonfinite_kernel(int rows, int cols, const S* X, int ldx, int lowerB, int* out) {
+  const size_t tot = (size_t)rows * cols;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % rows), j = (int)(e / rows);
+    if (!isfin(X[i + (size_t)j * ldx])) atomicMin(out, lowerB ? cols - 1 - j : j);
+  }
 }
 
 }  // namespace msy

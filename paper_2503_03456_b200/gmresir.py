@@ -133,7 +133,7 @@ def _precondition(W, f: _Factors):
     if info[0] == _native.SINGULAR_EQUATION:
         raise SingularEquationError(info[1], info[2])
     if info[0] == _native.NUMERIC_BREAKDOWN:
-        raise NumericBreakdownError("non-finite values in the triangular solve")
+        raise NumericBreakdownError(f"non-finite values while solving column {info[2]}")
     _gemm("N", f.UA, "N", V, tmp)
     out = torch.empty_like(W)
     _gemm("N", tmp, "C", f.UB, out)

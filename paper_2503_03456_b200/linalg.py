@@ -4,9 +4,11 @@
   mgs_qr   -> sylv_orth    (replaces linalg.py:252-273; Cholesky-QR, positive diagonal)
   gemm     -> sylv_gemm    (replaces linalg.py:125-154)
 
-``schur`` of a real matrix returns the REAL Schur form (quasi-triangular T
-with 2x2 blocks for complex-conjugate pairs, real U); pass
-``real_form=False`` to get the complex triangular form of the reference.
+``schur`` returns the reference's contract by default: a complex upper
+triangular T (strictly-lower part exactly zero) and unitary U.  Pass
+``real_form=True`` for a real input to get the real Schur form instead
+(quasi-triangular T with 2x2 blocks for complex-conjugate pairs, real U) --
+the form the solver itself uses internally.
 """
 
 from __future__ import annotations
@@ -65,7 +67,7 @@ def schur_tensor(A: torch.Tensor, info_out: list | None = None):
     return A, U
 
 
-def schur(A, ctx=None, real_form: bool | None = None, dev=None) -> SchurFactors:
+def schur(A, ctx=None, real_form: bool = False, dev=None) -> SchurFactors:
     """A = U T U^H in the context's precision (binary32 or binary64)."""
     A = as_matrix(A)
     m = A.shape[0]
@@ -73,7 +75,7 @@ def schur(A, ctx=None, real_form: bool | None = None, dev=None) -> SchurFactors:
         from .errors import DimensionError
         raise DimensionError("schur requires a square matrix")
     bits = _bits(ctx)
-    real = _is_real(A) if real_form is None else (real_form and _is_real(A))
+    real = bool(real_form) and _is_real(A)
     dt = {(True, 32): torch.float32, (True, 64): torch.float64,
           (False, 32): torch.complex64, (False, 64): torch.complex128}[(real, bits)]
     dev = D.device(dev)

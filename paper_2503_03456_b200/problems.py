@@ -150,3 +150,93 @@ def make(config: str, m: int | None = None, n: int | None = None,
     if config == "c4":
         return make_c4(index, m, seed)
     raise ValueError(f"unknown config {config!r}")
+
+
+# ---- the reference's ProblemGenerator kinds (cli.py:56-170), for harness and regime parity ----
+
+KRON_CAP = 4096  # DEFAULT_KRON_CAP, linalg.py:66
+_COND_CAP = {"normal": 6.0, "uniform": 15.0}  # transform condition caps (cli.py:104)
+_ATTEMPTS = 400
+
+
+@dataclass(frozen=True)
+class ProblemGenerator:
+    """Deterministic synthetic problem spec (cli.py:56-90): kinds random-dense,
+    logspace-conditioned (eigenvalues 10^linspace(0, t)), hermitian, lyapunov."""
+
+    kind: str
+    m: int
+    n: int
+    t: float = 0.0
+    seed: int = 0
+    stream: int = 0
+
+    def __post_init__(self):
+        if self.kind not in ("random-dense", "logspace-conditioned", "hermitian", "lyapunov"):
+            raise ValueError(f"unknown generator kind {self.kind!r}")
+        if self.kind == "lyapunov" and self.m != self.n:
+            raise ValueError("lyapunov generator requires m == n")
+        if self.t < 0:
+            raise ValueError("t must be nonnegative")
+
+
+def _with_spectrum(P: np.ndarray, lam: np.ndarray) -> np.ndarray:
+    """P diag(lam) P^{-1}, the inverse applied as a solve with P^T (cli.py:97-100)."""
+    return np.linalg.solve(P.T, (P * lam[None, :]).T).T
+
+
+def _transform(rng, k: int, family: str) -> np.ndarray:
+    """First draw whose 2-norm condition is under the family cap, else the best of the
+    attempts (cli.py:107-119); every rejection consumes the same stream."""
+    best, best_c = None, np.inf
+    for _ in range(_ATTEMPTS):
+        P = rng.standard_normal((k, k)) if family == "normal" else rng.random((k, k))
+        c = np.linalg.cond(P)
+        if c <= _COND_CAP[family]:
+            return P
+        if c < best_c:
+            best, best_c = P, c
+    return best
+
+
+def _logspace(rng, m: int, n: int, t: float):
+    """(A, B, C) with kappa_2(M_f) in [10^t, 10^(t+1)] while M_f is small enough to check
+    (cli.py:122-143); otherwise the first draw."""
+    checked = t >= 1.0 and m * n <= KRON_CAP
+    best, best_d = None, np.inf
+    for _ in range(_ATTEMPTS):
+        A = _with_spectrum(_transform(rng, m, "normal"), np.logspace(0.0, t, m))
+        B = _with_spectrum(_transform(rng, n, "uniform"), np.logspace(0.0, t, n))
+        C = rng.standard_normal((m, n))
+        if not checked:
+            return A, B, C
+        sv = np.linalg.svd(np.kron(np.eye(n), A) + np.kron(B.T, np.eye(m)), compute_uv=False)
+        kap = float(sv[0] / sv[-1])
+        if 10.0 ** t <= kap <= 10.0 ** (t + 1):
+            return A, B, C
+        d = abs(np.log10(kap) - (t + 0.5))
+        if d < best_d:
+            best, best_d = (A, B, C), d
+    return best
+
+
+def generate(g: ProblemGenerator) -> Problem:
+    """The reference's generate() (cli.py:146-170) on the same Philox stream."""
+    rng = rng_for(g.seed, g.stream)
+    m, n = g.m, g.n
+    if g.kind == "logspace-conditioned":
+        A, B, C = _logspace(rng, m, n, g.t)
+        return Problem(A, B, C, "general", "logspace", g.seed)
+    if g.kind == "random-dense":
+        A = rng.standard_normal((m, m))
+        B = rng.standard_normal((n, n))
+        return Problem(A, B, rng.standard_normal((m, n)), "general", "random-dense", g.seed)
+    if g.kind == "hermitian":
+        G = rng.standard_normal((m, m))
+        A = (G + G.T) / 2 + (1.0 + np.sqrt(m)) * np.eye(m)
+        G = rng.standard_normal((n, n))
+        B = (G + G.T) / 2 + (1.0 + np.sqrt(n)) * np.eye(n)
+        return Problem(A, B, rng.standard_normal((m, n)), "hermitian", "hermitian", g.seed)
+    A = rng.standard_normal((m, m)) + (1.0 + np.sqrt(m)) * np.eye(m)
+    G = rng.standard_normal((m, m))
+    return Problem(A, A.conj().T, (G + G.T) / 2, "lyapunov", "lyapunov", g.seed)

@@ -47,6 +47,11 @@ class RefinementConfig:
     u_h: FpFormat = field(default_factory=lambda: BINARY64)
     epsilon: float | None = None
     max_iter: int = 20
+    # Opt-in extension (not in the reference): the precision of the correction solve
+    # D_i = trsyl(T_A, T_B, R_i) inside Alg. 1.  None = u_h, the reference's choice
+    # (refinement.py:124); BINARY32 = the north star's fast mode (R_i and the iterate stay
+    # in binary64, only the triangular solve of the correction runs in binary32).
+    correction: FpFormat | None = None
 
     def __post_init__(self):
         if self.u_h.unit_roundoff > self.u_l.unit_roundoff:
@@ -55,6 +60,9 @@ class RefinementConfig:
             raise ValueError("epsilon must be positive")
         if self.max_iter < 1:
             raise ValueError("max_iter must be at least 1")
+        if self.correction is not None and format_bits(self.correction) not in (32, 64):
+            raise UnsupportedPrecisionError(
+                f"correction precision {self.correction.name} is not computed natively on B200")
 
     def resolve_epsilon(self, m: int, n: int) -> float:
         if self.epsilon is not None:
@@ -114,13 +122,13 @@ def _failure_string(rep: _native.Report):
     if rep.fail_stage == _native.STAGE_INITIAL:
         if s == _native.SINGULAR_EQUATION:
             return f"singular_equation at initial triangular solve: {pos}"
-        return "nan_breakdown at initial triangular solve: non-finite values in the initial solve"
+        return f"nan_breakdown at initial triangular solve: non-finite values while solving column {rep.fail_col}"
     if s == _native.SINGULAR_EQUATION:
         return f"singular_equation during refinement: {pos}"
     if s == _native.NUMERIC_BREAKDOWN:
         if rep.fail_stage == _native.STAGE_DIVERGED:
             return "nan_breakdown: iterate diverged to non-finite values"
-        return "nan_breakdown: non-finite values while solving the correction equation"
+        return f"nan_breakdown: non-finite values while solving column {rep.fail_col}"
     if s == _native.NON_CONVERGENCE:
         return "non_convergence: correction ratio above epsilon at max_iter"
     return None
@@ -181,6 +189,11 @@ def _solve_cm(A, B, C, X, m, n, kind, variant, low_bits, correction_bits, epsilo
     return rep
 
 
+def _correction_bits(cfg) -> int:
+    c = getattr(cfg, "correction", None)
+    return 64 if c is None else format_bits(c)
+
+
 def _run(p, cfg, variant, counter, y0_zero):
     if not hasattr(p, "A"):
         raise TypeError("expected a SylvesterProblem")
@@ -197,8 +210,8 @@ def _run(p, cfg, variant, counter, y0_zero):
     cv = (lambda M: D.to_cm(np.real(M) if real else M, dt, dev))
     tA, tB, tC = cv(p.A), cv(p.B), cv(p.C)
     tX = torch.empty_like(tC)
-    rep = _solve_cm(tA, tB, tC, tX, m, n, "lyapunov" if p.kind == "lyapunov" else "general", variant, lo, 64,
-                    eps, cfg.max_iter, y0_zero)
+    rep = _solve_cm(tA, tB, tC, tX, m, n, "lyapunov" if p.kind == "lyapunov" else "general", variant, lo,
+                    _correction_bits(cfg), eps, cfg.max_iter, y0_zero)
     _raise_for(rep.status)
     Xn = D.from_cm(tX).astype(np.complex128)
     if counter is not None:  # model-derived counts (costmodel.flops), see precision.FlopCounter

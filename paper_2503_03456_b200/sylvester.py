@@ -84,16 +84,30 @@ def residual(p, X, dev=None) -> float:
     return 0.0 if den == 0.0 else float(num / den)
 
 
+def _no_adjacent(offdiag: np.ndarray) -> bool:
+    """True when no two consecutive entries are nonzero (isolated 2x2 diagonal blocks)."""
+    nz = offdiag != 0
+    return not (nz[:-1] & nz[1:]).any()
+
+
 def _triangular_form(T: np.ndarray, allow_quasi: bool) -> str:
+    """The reference's test (sylvester.py:100-108) first: strictly triangular -> 'upper' /
+    'lower'.  Real quasi-triangular coefficients (isolated 2x2 diagonal blocks, the real
+    Schur form) are accepted only when ``allow_quasi`` and no two consecutive sub- (super-)
+    diagonal entries are nonzero; anything else (e.g. a Hessenberg matrix) is a
+    DimensionError, as in the reference."""
     n = T.shape[0]
     if n == 1:
         return "upper"
-    low = np.tril(T, -2 if allow_quasi else -1)
-    up = np.triu(T, 2 if allow_quasi else 1)
-    if not low.any():
+    if not np.tril(T, -1).any():
         return "upper"
-    if not up.any():
+    if not np.triu(T, 1).any():
         return "lower"
+    if allow_quasi:
+        if not np.tril(T, -2).any() and _no_adjacent(np.diag(T, -1)):
+            return "upper"
+        if not np.triu(T, 2).any() and _no_adjacent(np.diag(T, 1)):
+            return "lower"
     raise DimensionError("coefficient is not triangular")
 
 
@@ -134,7 +148,7 @@ def solve_sylv_tri(T_A, T_B, C, ctx=None, dev=None) -> np.ndarray:
     if info[0] == _native.SINGULAR_EQUATION:
         raise SingularEquationError(info[1], info[2])
     if info[0] == _native.NUMERIC_BREAKDOWN:
-        raise NumericBreakdownError("non-finite values in the triangular solve")
+        raise NumericBreakdownError(f"non-finite values while solving column {info[2]}")
     return D.from_cm(tW).astype(np.complex128)
 
 
@@ -180,7 +194,7 @@ def bartels_stewart(p, ctx=None, dev=None):
     if rep.status == _native.SINGULAR_EQUATION:
         raise SingularEquationError(rep.fail_row, rep.fail_col)
     if rep.status == _native.NUMERIC_BREAKDOWN:
-        raise NumericBreakdownError("non-finite values in the triangular solve")
+        raise NumericBreakdownError(f"non-finite values while solving column {rep.fail_col}")
     X = D.from_cm(tX).astype(np.complex128)
     return X, DirectSolveReport(float(rep.residual), None, None, float(rep.backward_error),
                                 dict(schur=rep.ms_schur, transform=rep.ms_setup, trsyl=rep.ms_y0,

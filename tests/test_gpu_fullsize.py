@@ -1,0 +1,178 @@
+"""Full-size parity of mp_orth / mp_inv on the B200 against the oracle, config by config.
+
+The reference answers are the committed fixtures tests/golden/full_<config>_<variant>.npz,
+produced by the bit-exact CPU oracle (the reference's own algorithm, pinned against the
+reference at small sizes) on the SAME seeded inputs (tests/golden/make_fullsize.py).
+
+North-star bars (BASELINE.json), each asserted here at full size:
+  * refinement iterations within +-1 of the reference's;
+  * normwise backward error ||C-AX-XB||_F/((||A||_F+||B||_F)||X||_F) <= 10x the reference's;
+  * relative solution difference <= 10 * kappa_sylv * u_64, with kappa_sylv = kappa_2 of the
+    Sylvester operator estimated matrix-free on the device (condition.kappa_sylv) and the
+    difference estimated through the fixture's Gaussian sketch X_ref @ Omega (16 columns);
+  * the first correction norm within [0.3, 3] of the reference's;
+  * C1: X symmetric to fp64 tolerance; C2: forward error against X_true no worse than 10x
+    the reference's own (both solve the same rounded C).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+U64 = 2.0 ** -53
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SKETCH_SEED, SKETCH_K = 777, 16
+
+
+def _fixture(config, variant):
+    path = os.path.join(GOLDEN, f"full_{config}_{variant}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    return np.load(path)
+
+
+@pytest.fixture(scope="module")
+def B200():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2503_03456_b200 as M
+    return M
+
+
+def backward(A, B, C, X):
+    return float(np.linalg.norm(A @ X + X @ B - C) / ((np.linalg.norm(A) + np.linalg.norm(B)) * np.linalg.norm(X)))
+
+
+def sketch_diff(X, XO_ref, real):
+    n = X.shape[1]
+    Om = np.random.default_rng(SKETCH_SEED).standard_normal((n, SKETCH_K))
+    Xs = X.real if real else X
+    return float(np.linalg.norm(Xs @ Om - XO_ref) / np.linalg.norm(XO_ref))
+
+
+_kappa_cache = {}
+
+
+def kappa_for(B200, config, A, B):
+    if config not in _kappa_cache:
+        _kappa_cache[config] = B200.kappa_sylv(A, B)
+    return _kappa_cache[config]
+
+
+def check_against(B200, g, pr, rep, config):
+    real = not pr.is_complex
+    X = rep.X.real if real else rep.X
+    assert rep.failure is None, rep.failure
+    assert rep.converged
+    assert abs(rep.iterations - int(g["iterations"])) <= 1, (rep.iterations, int(g["iterations"]))
+    be = backward(pr.A, pr.B, pr.C, X)
+    assert be <= 10 * max(float(g["backward"]), U64), (be, float(g["backward"]))
+    est = kappa_for(B200, config, pr.A, pr.B)
+    diff = sketch_diff(X, g["XO"], real)
+    assert diff <= 10 * est.kappa * U64, (diff, est.kappa)
+    d0, d0_ref = rep.correction_norms[0], float(g["correction_norms"][0])
+    assert 0.3 <= d0 / d0_ref <= 3.0, (d0, d0_ref)
+    assert abs(np.linalg.norm(X) - float(g["xnorm"])) <= 10 * est.kappa * U64 * float(g["xnorm"])
+    return dict(be=be, be_ref=float(g["backward"]), diff=diff, kappa=est.kappa, k=rep.iterations)
+
+
+@pytest.mark.parametrize("variant", ["orth", "inv"])
+@pytest.mark.parametrize("config", ["c0", "c1", "c2", "c3", "ch"])
+def test_fullsize_config(B200, config, variant):
+    from paper_2503_03456_b200 import problems as P
+    g = _fixture(config, variant)
+    pr = P.make(config, seed=0)
+    assert (pr.m, pr.n) == (int(g["m"]), int(g["n"]))
+    solver = B200.mp_orth if variant == "orth" else B200.mp_inv
+    rep = solver(B200.SylvesterProblem(pr.A, pr.B, pr.C, kind=pr.kind),
+                 B200.RefinementConfig(B200.BINARY32, B200.BINARY64))
+    info = check_against(B200, g, pr, rep, config)
+    X = rep.X.real if not pr.is_complex else rep.X
+    if pr.kind == "lyapunov":
+        assert np.linalg.norm(X - X.T) <= 10 * info["kappa"] * U64 * np.linalg.norm(X)
+    if pr.X_true is not None:
+        fwd = np.linalg.norm(X - pr.X_true) / np.linalg.norm(pr.X_true)
+        assert fwd <= 10 * max(float(g["fwd_true"]), info["kappa"] * U64), (fwd, float(g["fwd_true"]))
+    print(config, variant, info)
+
+
+@pytest.mark.parametrize("variant", ["orth", "inv"])
+def test_fullsize_c4_batch(B200, variant):
+    """C4 equations (m = n = 512) through the batched executor, each against its oracle fixture."""
+    import torch
+    from paper_2503_03456_b200 import problems as P
+    g = _fixture("c4", variant)
+    count = int(g["count"])
+    probs = [P.make_c4(i, 512) for i in range(count)]
+    A = torch.stack([torch.as_tensor(p.A) for p in probs]).cuda()
+    B = torch.stack([torch.as_tensor(p.B) for p in probs]).cuda()
+    C = torch.stack([torch.as_tensor(p.C) for p in probs]).cuda()
+    X, reps = B200.solve_batched(A, B, C, variant=variant)
+    Xh = X.cpu().numpy()
+    for i, p in enumerate(probs):
+        assert reps[i].status == 0
+        assert abs(reps[i].iterations - int(g[f"e{i}_iterations"])) <= 1
+        be = backward(p.A, p.B, p.C, Xh[i])
+        assert be <= 10 * max(float(g[f"e{i}_backward"]), U64), (i, be)
+        kap = B200.kappa_sylv(p.A, p.B).kappa
+        diff = sketch_diff(Xh[i], g[f"e{i}_XO"], True)
+        assert diff <= 10 * kap * U64, (i, diff, kap)
+
+
+@pytest.mark.parametrize("config,m,n", [("c0", 16, 12), ("c2", 24, 12), ("c3", 16, 16), ("c1", 20, 20),
+                                         ("c0", 40, 30)])
+def test_kappa_estimate_matches_kronecker(B200, config, m, n):
+    """The matrix-free estimate reproduces kappa_2(M_f) of the reference's Kronecker operator
+    (cli.py:261-268) where M_f can be formed."""
+    from paper_2503_03456_b200 import problems as P
+    pr = P.make(config, m, n, seed=3)
+    M = np.kron(np.eye(pr.n), pr.A) + np.kron(pr.B.T, np.eye(pr.m))
+    sv = np.linalg.svd(M, compute_uv=False)
+    est = B200.kappa_sylv(pr.A, pr.B, rtol=1e-8, max_iter=400)
+    assert est.sigma_max == pytest.approx(sv[0], rel=1e-3)
+    assert est.sigma_min == pytest.approx(sv[-1], rel=1e-3)
+    assert est.kappa == pytest.approx(sv[0] / sv[-1], rel=2e-3)
+    # default tolerance: a lower bound within a few percent
+    est = B200.kappa_sylv(pr.A, pr.B)
+    assert 0.9 * sv[0] / sv[-1] <= est.kappa <= 1.0001 * sv[0] / sv[-1]
+
+
+def test_kappa_estimate_singular_pair(B200):
+    """spec(A) meets spec(-B): sigma_min = 0, kappa infinite (sep_f returns 0, linalg.py:691-692)."""
+    A = np.array([[1.0, 2.0], [0.0, 3.0]])
+    B = np.array([[-1.0]])
+    est = B200.kappa_sylv(A, B)
+    assert est.sigma_min == 0.0 and est.kappa == float("inf")
+
+
+@pytest.mark.parametrize("config", ["c0", "c1", "c2", "c3", "ch"])
+def test_fullsize_fp32_correction_mode(B200, config):
+    """The north star's fast mode: the correction D_i solved in binary32 (RefinementConfig
+    .correction = BINARY32; the reference solves it in binary64, refinement.py:124).  Same
+    bars against the same oracle fixture as the reference-precision mode."""
+    from paper_2503_03456_b200 import problems as P
+    g = _fixture(config, "orth")
+    pr = P.make(config, seed=0)
+    cfg = B200.RefinementConfig(B200.BINARY32, B200.BINARY64, correction=B200.BINARY32)
+    rep = B200.mp_orth(B200.SylvesterProblem(pr.A, pr.B, pr.C, kind=pr.kind), cfg)
+    info = check_against(B200, g, pr, rep, config)
+    print(config, "fp32-correction", info)
+
+
+def test_fp32_correction_mode_batched_c4(B200):
+    import torch
+    from paper_2503_03456_b200 import problems as P
+    g = _fixture("c4", "orth")
+    probs = [P.make_c4(i, 512) for i in range(4)]
+    A = torch.stack([torch.as_tensor(p.A) for p in probs]).cuda()
+    B = torch.stack([torch.as_tensor(p.B) for p in probs]).cuda()
+    C = torch.stack([torch.as_tensor(p.C) for p in probs]).cuda()
+    X, reps = B200.solve_batched(A, B, C, correction_bits=32)
+    Xh = X.cpu().numpy()
+    for i, p in enumerate(probs):
+        assert reps[i].status == 0 and abs(reps[i].iterations - int(g[f"e{i}_iterations"])) <= 1
+        assert backward(p.A, p.B, p.C, Xh[i]) <= 10 * max(float(g[f"e{i}_backward"]), U64)
+        assert sketch_diff(Xh[i], g[f"e{i}_XO"], True) <= 10 * B200.kappa_sylv(p.A, p.B).kappa * U64

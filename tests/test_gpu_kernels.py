@@ -145,6 +145,22 @@ def test_trsyl_singular_pair_is_typed(B200):
     assert np.allclose(Y.ravel(), [0.95, 1.2])
 
 
+def test_trsyl_lower_bidiagonal_real_tb(B200, rng):
+    """A real lower-bidiagonal T_B is the reference's 'lower' form (descending columns), not a
+    quasi-triangular one; an upper-Hessenberg T_A is rejected like the reference does."""
+    m, n = 7, 5
+    TA = np.triu(rng.standard_normal((m, m))) + 4 * np.eye(m)
+    TB = np.diag(rng.standard_normal(n) + 3) + np.diag(rng.standard_normal(n - 1), -1)
+    C = rng.standard_normal((m, n))
+    Y = B200.solve_sylv_tri(TA, TB, C)
+    M = np.kron(np.eye(n), TA) + np.kron(TB.T, np.eye(m))
+    Yref = np.linalg.solve(M, C.flatten("F")).reshape((m, n), order="F")
+    assert np.abs(Y - Yref).max() <= 1e-12 * np.abs(Yref).max()
+    from paper_2503_03456_b200.errors import DimensionError
+    with pytest.raises(DimensionError):
+        B200.solve_sylv_tri(TA + np.diag(np.ones(m - 1), -1), TB, C)
+
+
 def _check_schur(A, sf, u, quasi):
     m = A.shape[0]
     T, U = sf.T, sf.U
@@ -168,7 +184,7 @@ def _check_schur(A, sf, u, quasi):
 def test_schur_real_fp32(B200, rng, m):
     from paper_2503_03456_b200 import BINARY32, PrecisionContext
     A = rng.standard_normal((m, m))
-    sf = B200.schur(A, PrecisionContext(BINARY32))
+    sf = B200.schur(A, PrecisionContext(BINARY32), real_form=True)
     _check_schur(A, sf, 2.0 ** -24, quasi=True)
 
 
@@ -186,7 +202,7 @@ def test_schur_binary64(B200, rng, m):
     limit at 100: multishift with async endgame blocks)."""
     from paper_2503_03456_b200 import BINARY64, PrecisionContext
     A = rng.standard_normal((m, m))
-    _check_schur(A, B200.schur(A, PrecisionContext(BINARY64)), 2.0 ** -53, quasi=True)
+    _check_schur(A, B200.schur(A, PrecisionContext(BINARY64), real_form=True), 2.0 ** -53, quasi=True)
     for mc in (40, 100):
         Ac = cmat(rng, mc, mc)
         _check_schur(Ac, B200.schur(Ac, PrecisionContext(BINARY64)), 2.0 ** -53, quasi=False)
@@ -201,6 +217,13 @@ def test_schur_reference_kats(B200, rng):
     sf = B200.schur(np.array([[0.0, 1.0], [-1.0, 0.0]]), ctx, real_form=False)
     got = np.sort_complex(np.diag(sf.T))
     assert np.abs(got - np.array([-1j, 1j])).max() < 1e-14
+    # the reference's default contract (pkg/tests/test_linalg.py): complex triangular T with an
+    # exactly zero strictly-lower part, also for real input
+    sf = B200.schur(np.array([[0.0, 1.0], [-1.0, 0.0]]), ctx)
+    assert np.abs(np.sort_complex(np.diag(sf.T)) - np.array([-1j, 1j])).max() < 1e-14
+    Ar = rng.standard_normal((17, 17))
+    sf = B200.schur(Ar, ctx)
+    assert (np.tril(sf.T, -1) == 0).all()
     A = np.eye(3, k=-1) + 0j  # companion of z^3 = 1: needs exceptional shifts
     A[0, 2] = 1.0
     sf = B200.schur(A, ctx, real_form=False)
@@ -212,7 +235,7 @@ def test_schur_reference_kats(B200, rng):
 def test_orth_cholesky_qr(B200, rng, m):
     from paper_2503_03456_b200 import BINARY32, PrecisionContext
     A = rng.standard_normal((m, m))
-    U = B200.schur(A, PrecisionContext(BINARY32)).U.real
+    U = B200.schur(A, PrecisionContext(BINARY32), real_form=True).U.real
     f = B200.mgs_qr(U)
     Q, R = f.Q.real, f.R.real
     assert np.linalg.norm(Q.T @ Q - np.eye(m)) < 1e-13 * m

@@ -140,3 +140,57 @@ def test_kernel_timer_abi_without_gpu():
     assert L.sylv_ktimer(2, n, c, ms, fl) == 0 and sum(c) == 0
     assert L.sylv_ktimer(0, n, c, ms, fl) == 0
     assert L.sylv_ktimer(7, n, c, ms, fl) == _native.EINVAL
+
+
+def test_triangular_form_follows_reference_test():
+    """sylvester.py:100-108: strictly triangular first; quasi forms only with isolated 2x2 blocks."""
+    from paper_2503_03456_b200.errors import DimensionError
+    from paper_2503_03456_b200.sylvester import _triangular_form
+    up = np.triu(np.ones((5, 5)))
+    assert _triangular_form(up, True) == "upper"
+    lo_bidiag = np.diag(np.ones(5)) + np.diag(np.ones(4), -1)
+    assert _triangular_form(lo_bidiag, True) == "lower"       # not mistaken for quasi-upper
+    quasi = up.copy()
+    quasi[1, 0] = quasi[4, 3] = 0.5
+    assert _triangular_form(quasi, True) == "upper"
+    assert _triangular_form(quasi.T, True) == "lower"
+    hess = up + np.diag(np.ones(4), -1)                        # consecutive subdiagonals
+    with pytest.raises(DimensionError):
+        _triangular_form(hess, True)
+    with pytest.raises(DimensionError):
+        _triangular_form(quasi, False)
+    with pytest.raises(DimensionError):
+        _triangular_form(np.ones((3, 3)), True)
+
+
+def test_batched_workspace_uses_effective_lanes():
+    """The workspace is sized for min(lanes, batch) lanes, not the 64-lane default (a 2-equation
+    batch at m=n=4096 must not ask for 64 lanes of workspace)."""
+    import ctypes as ct
+    from paper_2503_03456_b200 import _native
+    from paper_2503_03456_b200.batch import effective_lanes, _params
+    assert effective_lanes(0, 2) == 2 and effective_lanes(0, 500) == 64 and effective_lanes(8, 3) == 3
+    L = _native.lib()
+    p = _params(4096, 4096, False, "general", "orth", 32, 64, 1e-9, 20, False)
+    one, two = ct.c_size_t(), ct.c_size_t()
+    assert L.sylv_workspace_size(ct.byref(p), ct.byref(one)) == 0
+    assert L.sylv_batched_workspace_size(ct.byref(p), effective_lanes(0, 2), ct.byref(two)) == 0
+    assert two.value <= 2 * (one.value + 256)
+
+
+def test_generators_reproduce_reference_bytes():
+    """problems.generate == the reference's cli.generate, byte for byte (fixture digests made by
+    running the reference: tests/golden/make_golden_generators.py)."""
+    import hashlib
+    import json
+    from paper_2503_03456_b200.problems import ProblemGenerator, generate
+    with open(os.path.join(os.path.dirname(__file__), "golden", "generators.json")) as f:
+        fixtures = json.load(f)
+
+    def digest(M):
+        return hashlib.sha256(np.ascontiguousarray(np.asarray(M, dtype=np.complex128)).tobytes()).hexdigest()
+
+    for fx in fixtures:
+        p = generate(ProblemGenerator(*fx["spec"]))
+        assert (digest(p.A), digest(p.B), digest(p.C)) == (fx["A"], fx["B"], fx["C"]), fx["spec"]
+        assert p.kind == fx["kind"]
