@@ -779,10 +779,18 @@ int hess2_grid(int m) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = hess2_smem<S>(m);
   if (smem > 200 * 1024) return 0;
-  // static + dynamic smem may pass 48 KB even when the dynamic part does not
-  if (cudaFuncSetAttribute(hess_panel2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return 0;
+  // The attribute is a per-function ceiling shared by every thread: set it once to the largest
+  // size any m may need (setting it per call to this m's size races with the concurrent
+  // Schur(B) thread, whose launch would then exceed the ceiling).
+  {
+    static std::atomic<int> done{0};
+    if (!done.load(std::memory_order_acquire)) {
+      if (cudaFuncSetAttribute(hess_panel2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+          cudaSuccess)
+        return 0;
+      done.store(1, std::memory_order_release);
+    }
+  }
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hess_panel2_kernel<S>, HP_TPB, smem) != cudaSuccess)
     return 0;
   const int nslab = cdiv(m, HP_ROWS), units = nslab * cdiv(m, HP2_CW);
