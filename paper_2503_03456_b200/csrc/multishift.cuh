@@ -14,6 +14,7 @@
 //   * shifts: eigenvalues of the trailing ns x ns block (schur_small_kernel in
 //     eigenvalue mode), exceptional shifts after 6 stagnant sweeps.
 #pragma once
+#include <type_traits>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -46,6 +47,9 @@ constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
 // ops are branch-free (warp_left3 / warp_right3 redirect idle lanes to a dummy
 // row/column of the smem window).
 constexpr int KMAX = 8;  // bulge chains in flight per sweep (one CTA each)
+// fixed-trip, loads-first warp ops (wl3u / wr3u2) for real fp32 windows; the wider types keep
+// the loop forms (the unrolled register arrays would spill)
+template <class S> constexpr bool kFixedTrip = std::is_same<S, float>::value;
 template <class S>
 struct ChaseJobs {
   int ws[KMAX], we[KMAX], t0[KMAX], t1[KMAX];
@@ -54,7 +58,7 @@ struct ChaseJobs {
 };
 
 template <class S>
-__global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int hi, int nb, const ChaseJobs<S> jobs) {
+__global__ void __launch_bounds__(512) chase_kernel(S* H, int ldh, int lo, int hi, int nb, const ChaseJobs<S> jobs) {
   typedef typename tr<S>::R R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ws = jobs.ws[blockIdx.x], we = jobs.we[blockIdx.x], t0 = jobs.t0[blockIdx.x], t1 = jobs.t1[blockIdx.x];
@@ -109,8 +113,14 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
       refl3_fast(nr, x0, x1, x2, beta, tau, v1, v2);
       __syncwarp();
       if (!iszero(tau)) {
-        if (nr == 3) wl3<S, ld>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, v2, lane);
-        else wl2<S, ld>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, lane);
+        constexpr int NI = (MsCfg<S>::W + 31) / 32;
+        if constexpr (kFixedTrip<S>) {
+          if (nr == 3) wl3u<S, ld, NI>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, v2, lane);
+          else wl2u<S, ld, NI>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, lane);
+        } else {
+          if (nr == 3) wl3<S, ld>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, v2, lane);
+          else wl2<S, ld>(Hw, pl + 1, pl + 1, nw - 1, conj(tau), v1, lane);
+        }
       }
       if (p >= lo && lane == 0) {
         HW(pl + 1, pl) = beta;
@@ -125,7 +135,11 @@ __global__ void __launch_bounds__(768) chase_kernel(S* H, int ldh, int lo, int h
       // bottom, and every row beyond it is still an identity row of Z
       const int rmax = ((p + 4 < hi) ? p + 4 : hi) - ws;
       const int zmax = min(nw - 1, (lo - 1 + t) - ws + 3);
-      if (nr == 3) {
+      constexpr int NI = (MsCfg<S>::W + 31) / 32;
+      if constexpr (kFixedTrip<S>) {
+        if (nr == 3) wr3u2<S, ld, NI>(Hw, rmax, Zw, zmax, pl + 1, tau, v1, v2, lane);
+        else wr2u2<S, ld, NI>(Hw, rmax, Zw, zmax, pl + 1, tau, v1, lane);
+      } else if (nr == 3) {
         wr3<S, ld>(Hw, pl + 1, 0, rmax, tau, v1, v2, lane);
         wr3<S, ld>(Zw, pl + 1, 0, zmax, tau, v1, v2, lane);
       } else {

@@ -1091,8 +1091,12 @@ int sylv_schur(int dtype, int m, void* A, int lda, void* U, int ldu, void* ws, s
 int sylv_trsyl_workspace_size(int dtype, int m, int n, size_t* bytes) {
   if (!valid_dtype(dtype) || m < 1 || n < 1) return SYLV_EINVAL;
   Arena ar(nullptr, 0);
-  TrsylWs<float> w;
-  TrsylWs<float>::carve(ar, m, n, w);
+  switch (dtype) {  // the left-looking partials are sized by the element type
+    case 0: { TrsylWs<float> w; TrsylWs<float>::carve(ar, m, n, w); break; }
+    case 1: { TrsylWs<double> w; TrsylWs<double>::carve(ar, m, n, w); break; }
+    case 2: { TrsylWs<cfloat> w; TrsylWs<cfloat>::carve(ar, m, n, w); break; }
+    default: { TrsylWs<cdouble> w; TrsylWs<cdouble>::carve(ar, m, n, w); break; }
+  }
   ar.get<int>(8);
   ar.get<double>(3 * RED_BLOCKS + 16);
   *bytes = ar.off + 256;

@@ -17,6 +17,7 @@
 // element-level wavefront over 1x1/2x2 units.  (m/NB + n/NB - 1) launches total.
 #pragma once
 #include "common.cuh"
+#include "gemm_dmma.cuh"
 
 namespace msy {
 
@@ -25,10 +26,82 @@ namespace msy {
 // LEAF: 3 = lazy single-warp element wavefront (each unit gathers its row / column dot
 // products when it becomes ready: ~nru + ncu warp-synchronous steps, no block barriers);
 // 2 = two-level sub-tile wavefront; 1 = eager single-level wavefront (block barriers)
-template <class S> struct TrsylCfg { static constexpr int NB = 64; static constexpr int LEAF = 3; };
+#ifndef MSY_TRS_LEAF
+#define MSY_TRS_LEAF 3
+#endif
+template <class S> struct TrsylCfg { static constexpr int NB = 64; static constexpr int LEAF = MSY_TRS_LEAF; };
 template <> struct TrsylCfg<cdouble> { static constexpr int NB = 32; static constexpr int LEAF = 3; };
 
 enum { TRS_OK = 0, TRS_SINGULAR = 1, TRS_BREAKDOWN = 2 };
+
+// Reciprocal for the unit solves on the leaf's critical path: the hardware approximation
+// refined by Newton steps (two for fp64, one for fp32) -- a few dependent FMAs instead of
+// the IEEE division routine.  Callers handle exact zeros before calling.
+__device__ __forceinline__ float trs_rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+__device__ __forceinline__ double trs_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
+}
+template <class R> __device__ __forceinline__ cplx<R> trs_rcp(cplx<R> x) { return cplx<R>(R(1)) / x; }
+
+// Inverse of the p x q unit's Kronecker matrix  I (x) TA_RR + TB_CC^T (x) I  (unknowns ordered
+// r + PP c, as in unit_solve), by Gauss-Jordan with partial pivoting, written row-major into
+// out[0 .. (PP QQ)^2).  Returns false on an exactly zero pivot (the singular diagonal pair of
+// sylvester.py:141-143).  Precomputed for every unit pair of a leaf before its wavefront, so
+// the wavefront's per-unit solve is a small mat-vec.
+template <class S, int PP, int QQ>
+__device__ __forceinline__ bool unit_inverse(const S* As, const S* Bs, int P, int i, int j, S* out) {
+  typedef typename tr<S>::R R;
+  constexpr int NS = PP * QQ;
+  S M[NS][2 * NS];
+#pragma unroll
+  for (int c = 0; c < QQ; c++)
+#pragma unroll
+    for (int r = 0; r < PP; r++) {
+      const int u = r + PP * c;
+#pragma unroll
+      for (int v = 0; v < 2 * NS; v++) M[u][v] = (v == NS + u) ? S(1) : S(0);
+#pragma unroll
+      for (int r2 = 0; r2 < PP; r2++) M[u][r2 + PP * c] = M[u][r2 + PP * c] + As[(i + r) + (i + r2) * P];
+#pragma unroll
+      for (int c2 = 0; c2 < QQ; c2++) M[u][r + PP * c2] = M[u][r + PP * c2] + Bs[(j + c2) + (j + c) * P];
+    }
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < NS; c++) {
+#pragma unroll
+    for (int r = c + 1; r < NS; r++)
+      if (abs1(M[r][c]) > abs1(M[c][c]))
+#pragma unroll
+        for (int v = 0; v < 2 * NS; v++) { S t = M[c][v]; M[c][v] = M[r][v]; M[r][v] = t; }
+    if (abs1(M[c][c]) == R(0)) ok = false;
+    const S inv = ok ? S(1) / M[c][c] : S(0);
+#pragma unroll
+    for (int v = 0; v < 2 * NS; v++) M[c][v] = M[c][v] * inv;
+#pragma unroll
+    for (int r = 0; r < NS; r++) {
+      if (r == c) continue;
+      const S f = M[r][c];
+#pragma unroll
+      for (int v = 0; v < 2 * NS; v++) M[r][v] = M[r][v] - f * M[c][v];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NS; r++)
+#pragma unroll
+    for (int v = 0; v < NS; v++) out[r * NS + v] = M[r][NS + v];
+  return ok;
+}
+
+// leaf wavefront with 4 threads per unit (real types); complex keeps one thread per unit
+template <class S> constexpr bool kLeafGroups = std::is_same<S, float>::value || std::is_same<S, double>::value;
 
 // status: [0] = min key (crank*m + m-1-row) of a singular unit, INT_MAX if none
 __global__ void trsyl_status_init(int* status) {
@@ -120,7 +193,7 @@ __device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int 
       }
     }
     if (abs1(M[c][c]) == R(0)) ok = false;
-    const S inv = ok ? S(1) / M[c][c] : S(0);
+    const S inv = ok ? trs_rcp(M[c][c]) : S(0);
     dinv[c] = inv;
 #pragma unroll
     for (int r = c + 1; r < NS; r++) {
@@ -148,11 +221,267 @@ __device__ __forceinline__ bool unit_solve(const S* As, const S* Bs, S* Ws, int 
 #define MSY_TRS_MINB 2
 #endif
 constexpr int TRS_TPB = 256;  // 2 CTAs per SM: the update of one block overlaps another's loads
+// ---------------------------------------------------------------------------
+// Left-looking schedule (real types).  Tiles are at most TL_LD = 64 on a side (nominal
+// spacing 63, nudged +1 at a 2x2 block).  When tile (I, J) is due (anti-diagonal d) its
+// right-hand side is
+//   R = W[I, J] - T_A[I, i1:m] Y[i1:m, J] - Y[I, K_B] T_B[K_B, J],
+// K_B = [0, j0) for an upper T_B, [j1, n) for the lower (Lyapunov adjoint) one: all of
+// it already solved.  Both products are cut into K chunks of TL_KC; one CTA computes one
+// chunk of one tile into a private partial (trsyl_lpart_*), and the tile's leaf solve
+// subtracts the partials in chunk order (deterministic) before its wavefront.  Work per
+// solve is the same mn(m+n) flops as the eager schedule, but it runs as ~100 waves of
+// independent 64 x 64 x TL_KC GEMM tiles (fp64 on DMMA) instead of SIMT rank-64 updates,
+// and W is written once per tile.
+constexpr int TL_LD = 64, TL_TILE = TL_LD * TL_LD, TL_SPACING = TL_LD - 1, TL_KC = 256;
+
+// Chunks of a leaf, in the fixed summation order: [0] the tile just below (A part, solved on
+// the previous diagonal), [1] the tile just before in solve order (B part, previous diagonal),
+// then the older A-part range in TL_KC pieces, then the older B-part range.  The two "new"
+// chunks may be empty (zero partials).  The older chunks only read tiles solved two or more
+// diagonals back, so they are computed on a side stream while the previous diagonal solves.
+struct LeafK {
+  int na0, na1, nb0, nb1;   // new ranges [na0, na1) (A) and [nb0, nb1) (B)
+  int oa0, oa1, ob0, ob1;   // older ranges
+};
+__host__ __device__ __forceinline__ LeafK lleaf_ranges(int m, int n, int lowerB, int nbi, int nbj, const int* rb,
+                                                       const int* cb, int I, int J) {
+  LeafK k;
+  const int i1 = rb[I + 1];
+  k.na0 = i1;
+  k.na1 = I + 1 < nbi ? rb[I + 2] : m;
+  k.oa0 = k.na1;
+  k.oa1 = m;
+  if (!lowerB) {
+    const int j0 = cb[J];
+    k.nb1 = j0;
+    k.nb0 = J >= 1 ? cb[J - 1] : 0;
+    k.ob0 = 0;
+    k.ob1 = k.nb0;
+  } else {
+    const int j1 = cb[J + 1];
+    k.nb0 = j1;
+    k.nb1 = J + 1 < nbj ? cb[J + 2] : n;
+    k.ob0 = k.nb1;
+    k.ob1 = n;
+  }
+  return k;
+}
+__host__ __device__ __forceinline__ int lleaf_old_chunks(const LeafK& k) {
+  return (k.oa1 - k.oa0 + TL_KC - 1) / TL_KC + (k.ob1 - k.ob0 + TL_KC - 1) / TL_KC;
+}
+__host__ __device__ __forceinline__ int lleaf_chunks(const LeafK& k) { return 2 + lleaf_old_chunks(k); }
+
+// decode (leaf b of anti-diagonal d, chunk c) -> operand pointers and K range; false if idle
+template <class S>
+__device__ __forceinline__ bool lleaf_operands(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB,
+                                               const S* W, int ldw, const int* rb, const int* cb, int nbi, int nbj,
+                                               int d, int b, int c, int& bi, int& bj, const S*& Ap, int& ldA,
+                                               const S*& Bp, int& ldB, int& klen) {
+  const int llo = max(0, d - nbj + 1);
+  const int rI = llo + b, cJ = d - rI;
+  const int I = nbi - 1 - rI, J = lowerB ? nbj - 1 - cJ : cJ;
+  const int i0 = rb[I], i1 = rb[I + 1], j0 = cb[J], j1 = cb[J + 1];
+  bi = i1 - i0;
+  bj = j1 - j0;
+  if (bi <= 0 || bj <= 0) return false;
+  const LeafK k = lleaf_ranges(m, n, lowerB, nbi, nbj, rb, cb, I, J);
+  int a0, a1, isA;
+  if (c == 0) { a0 = k.na0; a1 = k.na1; isA = 1; }
+  else if (c == 1) { a0 = k.nb0; a1 = k.nb1; isA = 0; }
+  else {
+    c -= 2;
+    const int noa = (k.oa1 - k.oa0 + TL_KC - 1) / TL_KC, nob = (k.ob1 - k.ob0 + TL_KC - 1) / TL_KC;
+    if (c < noa) { a0 = k.oa0 + c * TL_KC; a1 = min(k.oa1, a0 + TL_KC); isA = 1; }
+    else if (c - noa < nob) { a0 = k.ob0 + (c - noa) * TL_KC; a1 = min(k.ob1, a0 + TL_KC); isA = 0; }
+    else return false;
+  }
+  klen = max(0, a1 - a0);
+  if (isA) {  // T_A[i0:i1, k] Y[k, j0:j1]
+    Ap = TA + i0 + (size_t)a0 * lda; ldA = lda;
+    Bp = W + a0 + (size_t)j0 * ldw; ldB = ldw;
+  } else {    // Y[i0:i1, k] T_B[k, j0:j1]
+    Ap = W + i0 + (size_t)a0 * ldw; ldA = ldw;
+    Bp = TB + a0 + (size_t)j0 * ldb; ldB = ldb;
+  }
+  return true;
+}
+
+// fp64 partial: 64 x 64 x klen on DMMA (4 warps, 32 x 32 per warp), staged like gemm_dmma_kernel
+__global__ void __launch_bounds__(128) trsyl_lpart_dmma_kernel(int m, int n, const double* __restrict__ TA, int lda,
+                                                               const double* __restrict__ TB, int ldb, int lowerB,
+                                                               const double* W, int ldw, const int* __restrict__ rb,
+                                                               const int* __restrict__ cb, int nbi, int nbj, int d,
+                                                               int maxch, int coff, double* __restrict__ part) {
+  int bi, bj, ldA, ldB, klen;
+  const double *Ap, *Bp;
+  const int chunk = blockIdx.y + coff;
+  if (!lleaf_operands<double>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, rb, cb, nbi, nbj, d, blockIdx.x, chunk, bi,
+                              bj, Ap, ldA, Bp, ldB, klen))
+    return;
+  __shared__ __align__(16) double As[2][DM_BK][DM_LD];
+  __shared__ __align__(16) double Bs[2][DM_BK][DM_LD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double ra[8], rbv[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int idx = tid + e * 128;
+      const int i = idx & 63, k = idx >> 6;            // A: 64 x 16, i fastest
+      ra[e] = (i < bi && k0 + k < klen) ? Ap[i + (size_t)(k0 + k) * ldA] : 0.0;
+      const int kk = idx & 15, j = idx >> 4;           // B: 16 x 64, k fastest
+      rbv[e] = (j < bj && k0 + kk < klen) ? Bp[(k0 + kk) + (size_t)j * ldB] : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int idx = tid + e * 128;
+      As[buf][idx >> 6][idx & 63] = ra[e];
+      Bs[buf][idx & 15][idx >> 4] = rbv[e];
+    }
+  };
+  const int nk = (klen + DM_BK - 1) / DM_BK;
+  load(0);
+  store(0);
+  __syncthreads();
+  const int fr = lane >> 2, fc = lane & 3;
+  for (int t = 0; t < nk; t++) {
+    const int cur = t & 1;
+    if (t + 1 < nk) load((t + 1) * DM_BK);
+#pragma unroll
+    for (int kk = 0; kk < DM_BK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) a[i] = As[cur][kk + fc][wm + i * 8 + fr];
+#pragma unroll
+      for (int j = 0; j < 4; j++) b[j] = Bs[cur][kk + fc][wn + j * 8 + fr];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    if (t + 1 < nk) store(cur ^ 1);
+    __syncthreads();
+  }
+  double* out = part + ((size_t)blockIdx.x * maxch + chunk) * TL_TILE;
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) out[(wm + i * 8 + fr) + (size_t)(wn + j * 8 + fc * 2 + h) * TL_LD] = acc[i][j][h];
+}
+
+// fp32 (and generic) partial: SIMT, 256 threads, 4 x 4 register tile each, K staged by 16
+template <class S>
+__global__ void __launch_bounds__(256) trsyl_lpart_simt_kernel(int m, int n, const S* __restrict__ TA, int lda,
+                                                               const S* __restrict__ TB, int ldb, int lowerB,
+                                                               const S* W, int ldw, const int* __restrict__ rb,
+                                                               const int* __restrict__ cb, int nbi, int nbj, int d,
+                                                               int maxch, int coff, S* __restrict__ part) {
+  int bi, bj, ldA, ldB, klen;
+  const S *Ap, *Bp;
+  const int chunk = blockIdx.y + coff;
+  if (!lleaf_operands<S>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, rb, cb, nbi, nbj, d, blockIdx.x, chunk, bi, bj,
+                         Ap, ldA, Bp, ldB, klen))
+    return;
+  constexpr int KS = 16;
+  __shared__ __align__(16) S As[2][KS][TL_LD + 4];
+  __shared__ __align__(16) S Bs[2][KS][TL_LD + 4];
+  const int tid = threadIdx.x, tr_ = tid & 15, tc = tid >> 4;
+  S acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b] = S(0);
+  S ra[4], rbv[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int idx = tid + e * 256;
+      const int i = idx & 63, k = idx >> 6;
+      ra[e] = (i < bi && k0 + k < klen) ? Ap[i + (size_t)(k0 + k) * ldA] : S(0);
+      const int kk = idx & 15, j = idx >> 4;
+      rbv[e] = (j < bj && k0 + kk < klen) ? Bp[(k0 + kk) + (size_t)j * ldB] : S(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int idx = tid + e * 256;
+      As[buf][idx >> 6][idx & 63] = ra[e];
+      Bs[buf][idx & 15][idx >> 4] = rbv[e];
+    }
+  };
+  const int nk = (klen + KS - 1) / KS;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < nk; t++) {
+    const int cur = t & 1;
+    if (t + 1 < nk) load((t + 1) * KS);
+#pragma unroll
+    for (int k = 0; k < KS; k++) {
+      S a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        a[q] = As[cur][k][tr_ + 16 * q];
+        b[q] = Bs[cur][k][tc + 16 * q];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int y = 0; y < 4; y++) acc[x][y] = fmac(a[x], b[y], acc[x][y]);
+    }
+    if (t + 1 < nk) store(cur ^ 1);
+    __syncthreads();
+  }
+  S* out = part + ((size_t)blockIdx.x * maxch + chunk) * TL_TILE;
+#pragma unroll
+  for (int x = 0; x < 4; x++)
+#pragma unroll
+    for (int y = 0; y < 4; y++) out[(tr_ + 16 * x) + (size_t)(tc + 16 * y) * TL_LD] = acc[x][y];
+}
+
+// W[tile] -= sum of the tile's partials, in chunk order (deterministic); grid (leaf, 16 slices)
+template <class S>
+__global__ void __launch_bounds__(256) trsyl_lreduce_kernel(int m, int n, int lowerB, S* W, int ldw,
+                                                            const int* __restrict__ rb, const int* __restrict__ cb,
+                                                            int nbi, int nbj, int d, int maxch,
+                                                            const S* __restrict__ part) {
+  const int llo = max(0, d - nbj + 1);
+  const int rI = llo + blockIdx.x, cJ = d - rI;
+  const int I = nbi - 1 - rI, J = lowerB ? nbj - 1 - cJ : cJ;
+  const int i0 = rb[I], i1 = rb[I + 1], j0 = cb[J], j1 = cb[J + 1];
+  const int e = blockIdx.y * 256 + threadIdx.x, i = e % TL_LD, j = e / TL_LD;
+  if (i >= i1 - i0 || j >= j1 - j0) return;
+  const int nch = lleaf_chunks(lleaf_ranges(m, n, lowerB, nbi, nbj, rb, cb, I, J));
+  const S* pp = part + (size_t)blockIdx.x * maxch * TL_TILE + e;
+  S acc = S(0);
+  int c = 0;
+  for (; c + 4 <= nch; c += 4) {  // four loads in flight, summed in chunk order
+    const S p0 = pp[(size_t)c * TL_TILE], p1 = pp[(size_t)(c + 1) * TL_TILE];
+    const S p2 = pp[(size_t)(c + 2) * TL_TILE], p3 = pp[(size_t)(c + 3) * TL_TILE];
+    acc = acc + p0; acc = acc + p1; acc = acc + p2; acc = acc + p3;
+  }
+  for (; c < nch; c++) acc = acc + pp[(size_t)c * TL_TILE];
+  S* w = W + (i0 + i) + (size_t)(j0 + j) * ldw;
+  *w = *w - acc;
+}
+
 template <class S>
 __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m, int n, const S* __restrict__ TA, int lda,
                                                          const S* __restrict__ TB, int ldb, int lowerB, S* W, int ldw,
                                                          const int* __restrict__ rb, const int* __restrict__ cb, int nbi,
-                                                         int nbj, int d, int* status, int dbg) {
+                                                         int nbj, int d, int* status, int dbg, int left = 0,
+                                                         S* __restrict__ uinv = nullptr) {
   constexpr int NB = TrsylCfg<S>::NB;
   constexpr int P = 4 * ((NB + 1 + 3) / 4);  // padded tile edge (smem stride)
   constexpr int TG = 16;                     // 16 x 16 threads, RM x RM accumulators each
@@ -226,7 +555,7 @@ __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m
   };
 
   // ---- updates from diagonal d-1 ----
-  if (d >= 1 && !(dbg & 2)) {
+  if (d >= 1 && !(dbg & 2) && !left) {
     // A-part: W -= TA[I, I*] Y[I*, J], with rank(I*) = d-1-cJ
     int ra = d - 1 - cJ;
     if (ra >= 0 && ra < rI) {
@@ -319,7 +648,163 @@ __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m
       g_n[1] = cnt;
     }
     __syncthreads();
-    if (warp < 2) {  // two warps run the wavefront, synchronised by a 64-thread named barrier
+    if constexpr (kLeafGroups<S>) {  // (real types always run the left-looking schedule: uinv is set)
+      // Lazy wavefront with GS = 4 threads per 1x1 / 2x2 unit: on step s every ready unit
+      // (row unit a, column unit s - a) gathers its two dot products (T_A rows below it x
+      // solved Y, solved Y left of it x T_B) split round-robin over its 4 threads, reduces
+      // them with two xor-shuffles, and its first thread solves the unit.  One block
+      // barrier per step; the dot products are ~4x shorter than with one thread per unit.
+      constexpr int GS = 4;
+      const int nru = g_n[0], ncu = g_n[1];
+      const int slot = tid / GS, sub = tid % GS;
+      // unit-pair inverses (16 entries per pair, pair a * ncu + b), all pairs in parallel;
+      // a zero pivot is flagged by a NaN first entry
+      S* minv = uinv + (size_t)blockIdx.x * TL_TILE * 16;
+      for (int e = tid; e < ((dbg & 16) ? 0 : nru * ncu); e += nt) {
+        const int a = e / ncu, b = e % ncu;
+        const int iu = g_rof[a], p = g_rln[a], ju = g_cof[b], q = g_cln[b];
+        S* o = minv + (size_t)e * 16;
+        bool ok;
+        if (p == 1 && q == 1) {
+          const S dd = As[iu + iu * P] + Bs[ju + ju * P];
+          ok = !iszero(dd);
+          o[0] = ok ? S(1) / dd : S(0);
+        } else if (p == 2 && q == 1) ok = unit_inverse<S, 2, 1>(As, Bs, P, iu, ju, o);
+        else if (p == 1 && q == 2) ok = unit_inverse<S, 1, 2>(As, Bs, P, iu, ju, o);
+        else ok = unit_inverse<S, 2, 2>(As, Bs, P, iu, ju, o);
+        if (!ok) o[0] = mk<S>(NAN, NAN);
+      }
+      __syncthreads();
+      // The units' inverses are staged two steps ahead into a 3-slot shared-memory ring with
+      // cp.async (the group of unit slot g copies the 16 entries of its unit of step s + 2), so
+      // the L2 latency of the table never sits on a step's critical path.
+      S* ring = Ws + (size_t)P * P;  // [3][64 slots][16]
+      auto stage = [&](int s2) {
+        const int a2 = max(0, s2 - ncu + 1) + slot;
+        if (s2 < nru + ncu - 1 && a2 <= min(s2, nru - 1)) {
+          const char* src = reinterpret_cast<const char*>(minv + (size_t)(a2 * ncu + (s2 - a2)) * 16);
+          char* dst = reinterpret_cast<char*>(ring + ((size_t)(s2 % 3) * 64 + slot) * 16);
+          constexpr int CH = 16 * (int)sizeof(S) / 16;  // 16-byte chunks per unit
+          for (int c = sub; c < CH; c += GS) {
+            const unsigned d = (unsigned)__cvta_generic_to_shared(dst + 16 * c);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 16 * c) : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      stage(0);
+      stage(1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      __syncthreads();
+      for (int s = 0; s < nru + ncu - 1; s++) {
+        const int a = max(0, s - ncu + 1) + slot;
+        const bool act = a <= min(s, nru - 1) && slot < (TRS_TPB / GS);
+        stage(s + 2);
+        S v00 = S(0), v10 = S(0), v01 = S(0), v11 = S(0);
+        int iu = 0, p = 1, ju = 0, q = 1;
+        if (act) {
+          const int bb = s - a;
+          iu = g_rof[a]; p = g_rln[a]; ju = g_cof[bb]; q = g_cln[bb];
+        }
+        if (act && !(dbg & 4)) {
+          const int kb = iu + p;
+          const int la = lowerB ? ju + q : 0, lb = lowerB ? bj : ju;
+          const int nr = bi - kb, nl = lb - la;
+          if (p == 1 && q == 1) {
+            S w0 = S(0), w1 = S(0);
+            int t = sub;
+            for (; t + GS < nr; t += 2 * GS) {
+              w0 = fmac(As[iu + (size_t)(kb + t) * P], Ws[(kb + t) + (size_t)ju * P], w0);
+              w1 = fmac(As[iu + (size_t)(kb + t + GS) * P], Ws[(kb + t + GS) + (size_t)ju * P], w1);
+            }
+            if (t < nr) w0 = fmac(As[iu + (size_t)(kb + t) * P], Ws[(kb + t) + (size_t)ju * P], w0);
+            t = sub;
+            for (; t + GS < nl; t += 2 * GS) {
+              w0 = fmac(Ws[iu + (size_t)(la + t) * P], Bs[(la + t) + (size_t)ju * P], w0);
+              w1 = fmac(Ws[iu + (size_t)(la + t + GS) * P], Bs[(la + t + GS) + (size_t)ju * P], w1);
+            }
+            if (t < nl) w0 = fmac(Ws[iu + (size_t)(la + t) * P], Bs[(la + t) + (size_t)ju * P], w0);
+            v00 = w0 + w1;
+          } else {
+            const int di = p > 1 ? 1 : 0, dj = q > 1 ? (int)P : 0;  // duplicates are discarded
+            // two independent accumulator sets, loads of both iterations issued together
+            S u00 = S(0), u10 = S(0), u01 = S(0), u11 = S(0);
+            int t = sub;
+            for (; t + GS < nr; t += 2 * GS) {
+              const S* X = As + iu + (size_t)(kb + t) * P;
+              const S* Y = Ws + (kb + t) + (size_t)ju * P;
+              const S* X2 = X + (size_t)GS * P;
+              const S* Y2 = Y + GS;
+              const S a0 = X[0], a1 = X[di], y0 = Y[0], y1 = Y[dj];
+              const S b0 = X2[0], b1 = X2[di], z0 = Y2[0], z1 = Y2[dj];
+              v00 = fmac(a0, y0, v00); v10 = fmac(a1, y0, v10); v01 = fmac(a0, y1, v01); v11 = fmac(a1, y1, v11);
+              u00 = fmac(b0, z0, u00); u10 = fmac(b1, z0, u10); u01 = fmac(b0, z1, u01); u11 = fmac(b1, z1, u11);
+            }
+            if (t < nr) {
+              const S* X = As + iu + (size_t)(kb + t) * P;
+              const S* Y = Ws + (kb + t) + (size_t)ju * P;
+              const S a0 = X[0], a1 = X[di], y0 = Y[0], y1 = Y[dj];
+              v00 = fmac(a0, y0, v00); v10 = fmac(a1, y0, v10); v01 = fmac(a0, y1, v01); v11 = fmac(a1, y1, v11);
+            }
+            t = sub;
+            for (; t + GS < nl; t += 2 * GS) {
+              const S* X = Ws + iu + (size_t)(la + t) * P;
+              const S* Y = Bs + (la + t) + (size_t)ju * P;
+              const S* X2 = X + (size_t)GS * P;
+              const S* Y2 = Y + GS;
+              const S a0 = X[0], a1 = X[di], y0 = Y[0], y1 = Y[dj];
+              const S b0 = X2[0], b1 = X2[di], z0 = Y2[0], z1 = Y2[dj];
+              v00 = fmac(a0, y0, v00); v10 = fmac(a1, y0, v10); v01 = fmac(a0, y1, v01); v11 = fmac(a1, y1, v11);
+              u00 = fmac(b0, z0, u00); u10 = fmac(b1, z0, u10); u01 = fmac(b0, z1, u01); u11 = fmac(b1, z1, u11);
+            }
+            if (t < nl) {
+              const S* X = Ws + iu + (size_t)(la + t) * P;
+              const S* Y = Bs + (la + t) + (size_t)ju * P;
+              const S a0 = X[0], a1 = X[di], y0 = Y[0], y1 = Y[dj];
+              v00 = fmac(a0, y0, v00); v10 = fmac(a1, y0, v10); v01 = fmac(a0, y1, v01); v11 = fmac(a1, y1, v11);
+            }
+            v00 = v00 + u00; v10 = v10 + u10; v01 = v01 + u01; v11 = v11 + u11;
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < GS; o <<= 1) {
+          v00 = v00 + __shfl_xor_sync(0xffffffffu, v00, o);
+          v10 = v10 + __shfl_xor_sync(0xffffffffu, v10, o);
+          v01 = v01 + __shfl_xor_sync(0xffffffffu, v01, o);
+          v11 = v11 + __shfl_xor_sync(0xffffffffu, v11, o);
+        }
+        if (act && !(dbg & 8)) {  // 4-way mat-vec: thread `sub` produces entry sub of the unit
+          const S* mi = ring + ((size_t)(s % 3) * 64 + slot) * 16;
+          const bool ok = !isnan(re(mi[0]));
+          const int ns = p * q;
+          S mcur[4];
+#pragma unroll
+          for (int c = 0; c < 4; c++) mcur[c] = (sub < ns && c < ns) ? mi[sub * ns + c] : S(0);
+          S r4[4];
+          r4[0] = Ws[iu + ju * P] - v00;
+          r4[1] = p == 2 ? Ws[(iu + 1) + ju * P] - v10 : S(0);
+          r4[2] = q == 2 ? Ws[iu + (ju + 1) * P] - v01 : S(0);
+          r4[3] = (p == 2 && q == 2) ? Ws[(iu + 1) + (ju + 1) * P] - v11 : S(0);
+          if (p == 1 && q == 2) r4[1] = r4[2];  // unknowns ordered r + p c
+          S y = S(0);
+#pragma unroll
+          for (int c = 0; c < 4; c++) y = fmac(mcur[c], r4[c], y);
+          __syncwarp(0xFu << (lane & ~3));  // the group's reads of W precede its writes
+          if (sub < ns) {
+            const int r = sub % p, c = sub / p;
+            Ws[(iu + r) + (ju + c) * P] = ok ? y : mk<S>(NAN, NAN);
+          }
+          if (!ok && sub == 0) {  // singular diagonal pair: report the first in reference order (decoded on the host)
+            const int jg = j0 + ju, ig = i0 + iu + p - 1;
+            const int crank = lowerB ? (n - 1 - jg) : jg;
+            atomicMin(&status[0], crank * m + (m - 1 - ig));
+          }
+        }
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // step s + 1's inverses have landed
+        __syncthreads();
+      }
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    } else if (warp < 2) {  // two warps run the wavefront, synchronised by a 64-thread named barrier
       const int nru = g_n[0], ncu = g_n[1];
       for (int s = 0; s < nru + ncu - 1; s++) {
         for (int a = tid; a < nru; a += 64) {
@@ -702,16 +1187,52 @@ __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m
 template <class S>
 static size_t trsyl_smem() {
   constexpr int P = 4 * ((TrsylCfg<S>::NB + 1 + 3) / 4);
-  return (size_t)3 * P * P * sizeof(S);
+  // + the 3 x 64 x 16 ring of staged unit inverses (grouped leaf, real types)
+  return (size_t)3 * P * P * sizeof(S) + (kLeafGroups<S> ? (size_t)3 * 64 * 16 * sizeof(S) : 0);
 }
+
+// side stream + events of the left-looking schedule (per host thread, like the sweep contexts)
+struct TrsylSide {
+  cudaStream_t side = nullptr;
+  cudaEvent_t evLeaf = nullptr, evOld = nullptr;
+  int dev = -1;
+};
+inline TrsylSide& trsyl_side() {
+  thread_local TrsylSide t;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (t.side == nullptr || t.dev != d) {
+    cudaStreamCreateWithFlags(&t.side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&t.evLeaf, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&t.evOld, cudaEventDisableTiming);
+    t.dev = d;
+  }
+  return t;
+}
+
+// left-looking schedule for the real types (fp32 Y0, fp64 corrections); complex keeps the
+// eager wavefront
+template <class S> constexpr bool kTrsylLeft = std::is_same<S, float>::value || std::is_same<S, double>::value;
 
 template <class S>
 struct TrsylWs {
   int* rb;
   int* cb;
+  S* part;    // left-looking split-K partials: [leaf][chunk][64 x 64]
+  S* uinv;    // per-leaf unit-pair inverses: [leaf][pair][16]
+  int maxch;  // chunks per leaf (upper bound)
   static void carve(Arena& ar, int m, int n, TrsylWs& w) {
     w.rb = ar.get<int>(m / 1 + 2);
     w.cb = ar.get<int>(n / 1 + 2);
+    w.part = nullptr;
+    w.uinv = nullptr;
+    w.maxch = 0;
+    if constexpr (kTrsylLeft<S>) {
+      const int nbi = cdiv(m, TL_SPACING), nbj = cdiv(n, TL_SPACING);
+      w.maxch = cdiv(m, TL_KC) + cdiv(n, TL_KC) + 4;  // + the two new chunks and two range tails
+      w.part = ar.get<S>((size_t)2 * std::min(nbi, nbj) * w.maxch * TL_TILE);  // x2: diagonal parity
+      w.uinv = ar.get<S>((size_t)std::min(nbi, nbj) * TL_TILE * 16);
+    }
   }
 };
 
@@ -723,6 +1244,71 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
   constexpr int NB = TrsylCfg<S>::NB;
   MSY_SMEM_ATTR_ONCE(trsyl_step_kernel<S>, (int)trsyl_smem<S>());
   static const int dbg = getenv("MSY_TRSYL_DBG") ? atoi(getenv("MSY_TRSYL_DBG")) : 0;
+  if constexpr (kTrsylLeft<S>) {
+    if (w.part != nullptr) {
+      const int nbi = cdiv(m, TL_SPACING), nbj = cdiv(n, TL_SPACING);
+      trsyl_partition_kernel<S><<<cdiv(max(nbi, nbj) + 1, 128), 128, 0, st>>>(m, TA, lda, n, TB, ldb, lowerB,
+                                                                              TL_SPACING, w.rb, nbi, w.cb, nbj);
+      MSY_LAUNCH_CK();
+      // Per diagonal d on `st`: the leaves' two "new" chunks (K <= 128 each), the fixed-order
+      // reduction into W, the leaf solves.  The older chunks of diagonal d + 1 run on the side
+      // stream during diagonal d (they read tiles solved by d - 1 at the latest).  Partials are
+      // double-buffered by diagonal parity.
+      TrsylSide& sd = trsyl_side();
+      const size_t half = (size_t)std::min(nbi, nbj) * w.maxch * TL_TILE;
+      auto leaves = [&](int d) { return std::min(d, nbi - 1) - std::max(0, d - nbj + 1) + 1; };
+      auto launch_part = [&](int d, int coff, int ny, cudaStream_t s2) -> int {
+        const int nl = leaves(d);
+        if (nl <= 0 || ny <= 0) return 0;
+        S* part = w.part + (d & 1) * half;
+        KScope ks(KC_TRSYL, 2.0 * TL_SPACING * TL_SPACING * TL_SPACING * (coff == 0 ? 2.0 : (d - 1.0)) * nl, s2);
+        if constexpr (std::is_same<S, double>::value)
+          trsyl_lpart_dmma_kernel<<<dim3(nl, ny), 128, 0, s2>>>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb, w.cb,
+                                                               nbi, nbj, d, w.maxch, coff, part);
+        else
+          trsyl_lpart_simt_kernel<S><<<dim3(nl, ny), 256, 0, s2>>>(m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb,
+                                                                   w.cb, nbi, nbj, d, w.maxch, coff, part);
+        MSY_LAUNCH_CK();
+        return 0;
+      };
+      // older chunks of diagonal d: K <= (d - 1) * 64 in TL_KC pieces (+2 for the two ranges' tails)
+      auto old_chunks = [&](int d) { return d >= 2 ? std::min(w.maxch - 2, cdiv((d - 1) * TL_LD, TL_KC) + 2) : 0; };
+      MSY_CK(cudaEventRecord(sd.evLeaf, st));  // "leaf(-1)": the partition is done
+      for (int d = 0; d < nbi + nbj - 1; d++) {
+        const int nleaf = leaves(d);
+        if (nleaf <= 0) continue;
+        if (d > 0) MSY_CK(cudaStreamWaitEvent(st, sd.evOld, 0));   // old chunks of d (issued last iteration)
+        // side: old chunks of d + 1 after leaf(d - 1) (recorded at the end of the last iteration)
+        cudaStream_t side = (dbg & 32) ? st : sd.side;  // dbg 32: serialise (A/B of the overlap)
+        MSY_CK(cudaStreamWaitEvent(side, sd.evLeaf, 0));
+        int rc = launch_part(d + 1, 2, d + 1 < nbi + nbj - 1 ? old_chunks(d + 1) : 0, side);
+        if (rc) return rc;
+        MSY_CK(cudaEventRecord(sd.evOld, side));
+        if (d > 0) {
+          if (d == 1) {  // diagonal 1 has no older chunks; its new ones
+            rc = launch_part(d, 0, 2, st);
+          } else {
+            rc = launch_part(d, 0, 2, st);
+          }
+          if (rc) return rc;
+          KScope ks(KC_TRSYL, 0, st);
+          trsyl_lreduce_kernel<S><<<dim3(nleaf, TL_TILE / 256), 256, 0, st>>>(m, n, lowerB, W, ldw, w.rb, w.cb, nbi,
+                                                                              nbj, d, w.maxch,
+                                                                              w.part + (d & 1) * half);
+          MSY_LAUNCH_CK();
+        }
+        {
+          KScope ks(KC_TRSYL, 0, st);
+          trsyl_step_kernel<S><<<(unsigned)nleaf, TRS_TPB, trsyl_smem<S>(), st>>>(
+              m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb, w.cb, nbi, nbj, d, status, dbg & ~3, 1, w.uinv);
+          MSY_LAUNCH_CK();
+        }
+        MSY_CK(cudaEventRecord(sd.evLeaf, st));
+      }
+      MSY_CK(cudaStreamWaitEvent(st, sd.evOld, 0));  // join the side stream
+      return 0;
+    }
+  }
   const int nbi = cdiv(m, NB), nbj = cdiv(n, NB);
   trsyl_partition_kernel<S><<<cdiv(max(nbi, nbj) + 1, 128), 128, 0, st>>>(m, TA, lda, n, TB, ldb, lowerB, NB, w.rb,
                                                                           nbi, w.cb, nbj);
