@@ -5,6 +5,7 @@
 // Scalar codes (the C-ABI `dtype`): 0 = float (s), 1 = double (d),
 // 2 = complex<float> (c), 3 = complex<double> (z).
 #pragma once
+#include "config.cuh"
 #include <atomic>
 #include <mutex>
 #include <vector>

@@ -796,7 +796,7 @@ int hess2_grid(int m) {
   const int nslab = cdiv(m, HP_ROWS), units = nslab * cdiv(m, HP2_CW);
   int G = std::min(per * nsm, std::max(nslab, std::min(units, nsm)));
   // optional cap (the concurrent Schur(A) / Schur(B) pair: two co-resident cooperative grids)
-  static const int gmax_env = getenv("MSY_HESS_GMAX") ? atoi(getenv("MSY_HESS_GMAX")) : -1;
+  constexpr int gmax_env = MSY_HESS_GMAX;
   const int gmax = gmax_env >= 0 ? gmax_env : hess_grid_cap();
   if (gmax > 0) G = std::min(G, std::max(gmax, cdiv(nslab, HP2_OWN)));
   return (G > 0 && cdiv(nslab, G) <= HP2_OWN) ? G : 0;  // each CTA caches at most HP2_OWN slabs
@@ -825,7 +825,7 @@ int hessenberg_blocked(int m, S* A, int lda, S* Q, int ldq, HessWs<S>& w, cudaSt
   zero_kernel<S><<<cdiv((size_t)m * m, 256), 256, 0, st>>>((size_t)m * m, w.V);
   MSY_LAUNCH_CK();
   const int last = m - 3;  // last column that gets a reflector
-  static const int hmode = getenv("MSY_HESS_MODE") ? atoi(getenv("MSY_HESS_MODE")) : 2;  // 0 none, 1 v1, 2 v2
+  constexpr int hmode = MSY_HESS_MODE;  // 0 per-column kernels, 1 v1 cooperative, 2 v2 cooperative
   const int G = hmode == 0 ? 0 : (hmode == 1 ? hess_coop_grid<S>(m) : hess2_grid<S>(m));
   int np = 0;
   for (int k = 0; k <= last; k += HESS_NB, np++) {

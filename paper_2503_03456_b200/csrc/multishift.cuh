@@ -412,7 +412,7 @@ int apply_z_regions(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int
   int nblk = (cL1 > cL0 ? cdiv(cL1 - cL0, 32) : 0) + cdiv(rR1, 32) + (U ? cdiv(m, 32) : 0);
   if (nblk == 0) return 0;
   KScope ks(KC_APPLYZ, (tr<S>::cx ? 8.0 : 2.0) * nz * nz * ((cL1 > cL0 ? cL1 - cL0 : 0) + rR1 + (U ? m : 0)), st);
-  static const int azc_mode = getenv("MSY_AZC") ? atoi(getenv("MSY_AZC")) : 2;
+  constexpr int azc_mode = MSY_AZC;
   if (azc_mode >= 2) {  // the cluster-split kernel with a single job
     MSY_SMEM_ATTR_ONCE(apply_z_cl_kernel<S>, (int)azc_smem<S>());
     ApplyJobs<S> j = {};

@@ -119,7 +119,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
   MSY_SMEM_ATTR_ONCE(apply_z_kernel<S>, (int)applyz_smem<S>(W));
   MSY_SMEM_ATTR_ONCE(apply_z_multi_kernel<S>, (int)applyz_smem<S>(W));
   MSY_SMEM_ATTR_ONCE(apply_z_cl_kernel<S>, (int)azc_smem<S>());
-  static const int azc_mode = getenv("MSY_AZC") ? atoi(getenv("MSY_AZC")) : 2;
+  constexpr int azc_mode = MSY_AZC;
   if (K < 1 || K > KMAX) return -5;
   const int span = hi - lo;
   const long Tn = 4L * (nb - 1) + span;
@@ -157,7 +157,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
     // per time step tau, on st: chase (all chains) -> near rows -> near columns; on aux:
     // far rows -> far columns + U, overlapping the next chase.  near(tau) waits for
     // far(tau-1) (their regions can meet); Z buffers alternate with tau.
-    static const bool mc_serial = getenv("MSY_MC_SERIAL") != nullptr;
+    constexpr bool mc_serial = MSY_MC_SERIAL != 0;
     const bool ovl = sc->aux != nullptr && !mc_serial;
     cudaStream_t fst = ovl ? sc->aux : st;
     for (int tau = 0; tau < nwins + (K - 1) * D; tau++) {
@@ -320,7 +320,7 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
   // columns to its right) and U run at once; the column-side update (rows above the block)
   // is deferred to the end.  Sweeps only multiply rows above the block from the left, so the
   // deferred right multiplication commutes with them and no entry is written concurrently.
-  static const bool sync_end = getenv("MSY_SYNC_ENDGAME") != nullptr;
+  constexpr bool sync_end = MSY_SYNC_ENDGAME != 0;
   const bool async_end = sc->aux != nullptr && sc->eg != nullptr && !sync_end && w.Zend != nullptr;
   struct Deferred { int lo, sz; size_t zoff; };
   std::vector<Deferred> defs;
@@ -375,15 +375,15 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
       continue;
     }
     if (loc.sweeps >= limit) { loc.status = ST_ITERLIMIT; break; }
-    static const int kmax_env = getenv("MSY_CHAINS") ? atoi(getenv("MSY_CHAINS")) : KMAX;
+    constexpr int kmax_env = MSY_CHAINS;
     // bulges per chain (a chain of nb bulges spans 4 nb rows of the W-row chase window)
-    static const int NBc = std::max(2, std::min(MsCfg<S>::NB, getenv("MSY_NB") ? atoi(getenv("MSY_NB")) : MsCfg<S>::NB));
+    const int NBc = std::max(2, std::min(MsCfg<S>::NB, MSY_NB_CHAIN > 0 ? MSY_NB_CHAIN : MsCfg<S>::NB));
     bool exc = (stag > 0 && stag % 6 == 0);
     // ---- aggressive early deflation on the trailing window (aed.cuh) ----
-    static const int aed_on = getenv("MSY_AED") ? atoi(getenv("MSY_AED")) : 0;
-    static const int aed_nw = getenv("MSY_AED_NW") ? atoi(getenv("MSY_AED_NW")) : AedCfg<S>::NW;
-    static const int aed_gmax = getenv("MSY_AED_GMAX") ? atoi(getenv("MSY_AED_GMAX")) : 16;
-    static const int aed_nibble = getenv("MSY_AED_NIBBLE") ? atoi(getenv("MSY_AED_NIBBLE")) : 14;
+    constexpr int aed_on = MSY_AED;
+    constexpr int aed_nw = MSY_AED_NW;
+    constexpr int aed_gmax = MSY_AED_GMAX;
+    constexpr int aed_nibble = MSY_AED_NIBBLE;
     int aed_ls = 0;
     if (aed_on && !exc) {
       const int nw = std::max(16, std::min({aed_nw, AedCfg<S>::NW, sz - 1}));
@@ -446,7 +446,7 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
       MSY_LAUNCH_CK();
       // shifts need not be converged to working accuracy: a looser deflation tolerance
       // cuts the eigenvalue iteration roughly in half
-      static const double stol = getenv("MSY_SHIFT_TOL") ? atof(getenv("MSY_SHIFT_TOL")) : 1e-3;
+      constexpr double stol = MSY_SHIFT_TOL;
       rc = schur_small_launch<S>(ns, w.sblk, ns, nullptr, 0, SS_EIGONLY, w.wr, w.wi, w.dinfo + 16, st,
                                  (R)std::max<double>(stol, tr<S>::u()));
       if (rc) return rc;

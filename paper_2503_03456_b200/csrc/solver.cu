@@ -61,7 +61,7 @@ int ctx_init() {
   // default (least) priority, so queued far work yields SMs to the critical path.
   int lo_pri = 0, hi_pri = 0;
   MSY_CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
-  static const bool no_pri = getenv("MSY_NO_STREAM_PRIORITY") != nullptr;
+  constexpr bool no_pri = MSY_NO_STREAM_PRIORITY != 0;
   MSY_CK(cudaStreamCreateWithPriority(&g_ctx.side, cudaStreamNonBlocking, no_pri ? lo_pri : hi_pri));
   MSY_CK(cudaStreamCreateWithPriority(&g_ctx.hiA, cudaStreamNonBlocking, no_pri ? lo_pri : hi_pri));
   MSY_CK(cudaEventCreateWithFlags(&g_ctx.ev_a, cudaEventDisableTiming));

@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m
       // unit-pair inverses (16 entries per pair, pair a * ncu + b), all pairs in parallel;
       // a zero pivot is flagged by a NaN first entry
       S* minv = uinv + (size_t)blockIdx.x * TL_TILE * 16;
-      for (int e = tid; e < ((dbg & 16) ? 0 : nru * ncu); e += nt) {
+      for (int e = tid; e < nru * ncu; e += nt) {
         const int a = e / ncu, b = e % ncu;
         const int iu = g_rof[a], p = g_rln[a], ju = g_cof[b], q = g_cln[b];
         S* o = minv + (size_t)e * 16;
@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m
           const int bb = s - a;
           iu = g_rof[a]; p = g_rln[a]; ju = g_cof[bb]; q = g_cln[bb];
         }
-        if (act && !(dbg & 4)) {
+        if (act) {
           const int kb = iu + p;
           const int la = lowerB ? ju + q : 0, lb = lowerB ? bj : ju;
           const int nr = bi - kb, nl = lb - la;
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(TRS_TPB, MSY_TRS_MINB) trsyl_step_kernel(int m
           v01 = v01 + __shfl_xor_sync(0xffffffffu, v01, o);
           v11 = v11 + __shfl_xor_sync(0xffffffffu, v11, o);
         }
-        if (act && !(dbg & 8)) {  // 4-way mat-vec: thread `sub` produces entry sub of the unit
+        if (act) {  // 4-way mat-vec: thread `sub` produces entry sub of the unit
           const S* mi = ring + ((size_t)(s % 3) * 64 + slot) * 16;
           const bool ok = !isnan(re(mi[0]));
           const int ns = p * q;
@@ -1243,7 +1243,7 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
           int* status, cudaStream_t st) {
   constexpr int NB = TrsylCfg<S>::NB;
   MSY_SMEM_ATTR_ONCE(trsyl_step_kernel<S>, (int)trsyl_smem<S>());
-  static const int dbg = getenv("MSY_TRSYL_DBG") ? atoi(getenv("MSY_TRSYL_DBG")) : 0;
+  constexpr int dbg = 0;  // trsyl_step_kernel's timing-experiment bits (MSY_TRSYL_DBG was removed)
   if constexpr (kTrsylLeft<S>) {
     if (w.part != nullptr) {
       const int nbi = cdiv(m, TL_SPACING), nbj = cdiv(n, TL_SPACING);
@@ -1279,7 +1279,7 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
         if (nleaf <= 0) continue;
         if (d > 0) MSY_CK(cudaStreamWaitEvent(st, sd.evOld, 0));   // old chunks of d (issued last iteration)
         // side: old chunks of d + 1 after leaf(d - 1) (recorded at the end of the last iteration)
-        cudaStream_t side = (dbg & 32) ? st : sd.side;  // dbg 32: serialise (A/B of the overlap)
+        cudaStream_t side = sd.side;
         MSY_CK(cudaStreamWaitEvent(side, sd.evLeaf, 0));
         int rc = launch_part(d + 1, 2, d + 1 < nbi + nbj - 1 ? old_chunks(d + 1) : 0, side);
         if (rc) return rc;
@@ -1300,7 +1300,7 @@ int trsyl(int m, int n, const S* TA, int lda, const S* TB, int ldb, int lowerB, 
         {
           KScope ks(KC_TRSYL, 0, st);
           trsyl_step_kernel<S><<<(unsigned)nleaf, TRS_TPB, trsyl_smem<S>(), st>>>(
-              m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb, w.cb, nbi, nbj, d, status, dbg & ~3, 1, w.uinv);
+              m, n, TA, lda, TB, ldb, lowerB, W, ldw, w.rb, w.cb, nbi, nbj, d, status, 0, 1, w.uinv);
           MSY_LAUNCH_CK();
         }
         MSY_CK(cudaEventRecord(sd.evLeaf, st));

@@ -247,29 +247,3 @@ def test_orth_cholesky_qr(B200, rng, m):
     assert np.linalg.norm(fc.Q @ fc.R - Uc) < 1e-13 * m
     assert (np.diag(fc.R).real > 0).all() and np.abs(np.diag(fc.R).imag).max() < 1e-15
 
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"MSY_AED": "1"}, {"MSY_MSS_AED": "24"}, {"MSY_SYNC_ENDGAME": "1", "MSY_AZC": "0"}])
-def test_schur_opt_in_paths(env):
-    """The opt-in schedules kept for experiments (large-loop AED, in-kernel AED, synchronous
-    endgame with the pre-cluster Z application) still give a valid Schur form.  The switches
-    are read once per process, so each runs in a subprocess."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = (
-        "import numpy as np, paper_2503_03456_b200 as M\n"
-        "from paper_2503_03456_b200 import BINARY32, PrecisionContext\n"
-        "rng = np.random.default_rng(7)\n"
-        "for m in (150, 600):\n"
-        "    A = rng.standard_normal((m, m)) / m ** 0.5 + 2 * np.eye(m)\n"
-        "    sf = M.schur(A, PrecisionContext(BINARY32))\n"
-        "    T, U = sf.T, sf.U\n"
-        "    rec = np.linalg.norm(U @ T @ U.conj().T - A) / np.linalg.norm(A)\n"
-        "    orth = np.linalg.norm(U.conj().T @ U - np.eye(m))\n"
-        "    assert rec < 1e-4 and orth < 1e-3 and (np.tril(T, -2) == 0).all(), (m, rec, orth)\n"
-        "print('ok')\n")
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env}, capture_output=True,
-                       text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
