@@ -160,6 +160,13 @@ int sylv_orth(int dtype, int m, const void* U, int ldu, void* Q, int ldq, void* 
 int sylv_gemm(int dtype, char opa, char opb, int m, int n, int k, const void* alpha, const void* A, int lda,
               const void* B, int ldb, const void* beta, void* C, int ldc, void* stream);
 
+/* solve_hermitian (sylvester.py:181-196), its entrywise step: W[i,j] /= dA[i] + dB[j] for the
+ * real eigenvalues dA (m) and dB (n) of the Hermitian coefficients (device arrays, double);
+ * dtype 1 or 3.  ws: >= 4 bytes of device scratch.  info[0] = SYLV_SINGULAR_EQUATION with
+ * info[1..2] = (i, j) of the first exactly zero denominator in row-major order, else SYLV_OK. */
+int sylv_hdiv(int dtype, int m, int n, const double* dA, const double* dB, void* W, int ldw, void* ws,
+              size_t ws_bytes, void* stream, int* info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,6 +24,7 @@ from .batch import gather_solutions, shard_range, solve_batched
 from .sylvester import DirectSolveReport, SylvesterProblem, bartels_stewart, residual, solve_sylv_tri
 from .linalg import QrFactors, SchurFactors, gemm, mgs_qr, schur
 from .condition import KappaEstimate, kappa_sylv, kappa_sylv_tensor
+from .hermitian import hermitian_eig, solve_hermitian
 from .gmresir import GmresConfig, GmresIrReport, apply_preconditioner, gmres_ir_sylv
 
 __version__ = "0.1.0"

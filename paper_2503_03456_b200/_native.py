@@ -28,7 +28,7 @@ EXPORTS = (
     "sylv_version", "sylv_status_string", "sylv_launch_count", "sylv_microbench", "sylv_ktimer",
     "sylv_workspace_size", "sylv_solve", "sylv_batched_workspace_size", "sylv_solve_batched",
     "sylv_refine_workspace_size", "sylv_refine", "sylv_schur_workspace_size", "sylv_schur",
-    "sylv_trsyl_workspace_size", "sylv_trsyl", "sylv_orth_workspace_size", "sylv_orth", "sylv_gemm",
+    "sylv_trsyl_workspace_size", "sylv_trsyl", "sylv_orth_workspace_size", "sylv_orth", "sylv_gemm", "sylv_hdiv",
 )
 
 
@@ -91,6 +91,7 @@ def lib():
         L.sylv_orth_workspace_size.argtypes = [ip, ip, ct.POINTER(sz)]
         L.sylv_orth.argtypes = [ip, ip, vp, ip, vp, ip, vp, ip, vp, sz, vp, ct.POINTER(ct.c_int)]
         L.sylv_gemm.argtypes = [ip, ct.c_char, ct.c_char, ip, ip, ip, vp, vp, ip, vp, ip, vp, vp, ip, vp]
+        L.sylv_hdiv.argtypes = [ip, ip, ip, vp, vp, vp, ip, vp, sz, vp, ct.POINTER(ct.c_int)]
         _lib = L
     return _lib
 

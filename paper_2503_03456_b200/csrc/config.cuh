@@ -54,3 +54,6 @@
 #ifndef MSY_NO_STREAM_PRIORITY
 #define MSY_NO_STREAM_PRIORITY 0
 #endif
+#ifndef MSY_LANE_HESS_CAP
+#define MSY_LANE_HESS_CAP 0    // cap on each batched lane's cooperative Hessenberg grid (0: none)
+#endif

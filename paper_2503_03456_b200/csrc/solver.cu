@@ -934,6 +934,9 @@ int sylv_solve_batched(const sylv_params* p, int batch, const void* const* A, in
     }
     host_sync_blocking() = true;
     t_serial_lane = true;
+    // many lanes' cooperative Hessenberg panels must be co-resident: small grids per lane
+    const int cap_saved = hess_grid_cap();
+    hess_grid_cap() = MSY_LANE_HESS_CAP;
     cudaStreamWaitEvent(ls.st, start, 0);
     char* mine = (char*)ws + one * (size_t)lane;
     for (int i; (i = next.fetch_add(1)) < batch && err.load() == 0;) {
@@ -944,6 +947,7 @@ int sylv_solve_batched(const sylv_params* p, int batch, const void* const* A, in
     done[lane] = ls.done;
     host_sync_blocking() = false;
     t_serial_lane = false;
+    hess_grid_cap() = cap_saved;
   };
   LanePool::get().run(nl, fn);
   for (int l = 0; l < nl; l++)
@@ -1195,5 +1199,46 @@ int sylv_gemm(int dtype, char opa, char opb, int m, int n, int k, const void* al
     default: return gemm<cdouble>(opa, opb, m, n, k, *(const cdouble*)alpha, (const cdouble*)A, lda,
                                   (const cdouble*)B, ldb, *(const cdouble*)beta, (cdouble*)C, ldc, st);
   }
+}
+
+// ---- Hermitian fast path: entrywise division by the eigenvalue sums ---------------
+// W[i, j] /= dA[i] + dB[j] (solve_hermitian, sylvester.py:181-196); the first exactly zero
+// denominator in row-major order (np.argwhere(denom == 0)[0]) is reported in info[1..2].
+template <class S>
+__global__ void hdiv_kernel(int m, int n, const double* __restrict__ dA, const double* __restrict__ dB, S* W, int ldw,
+                            int* first_zero) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  for (int jj = j; jj < n; jj += gridDim.y) {
+    if (i >= m) continue;
+    const double d = dA[i] + dB[jj];
+    if (d == 0.0) atomicMin(first_zero, i * n + jj);
+    S* w = W + i + (size_t)jj * ldw;
+    *w = *w * S(1.0 / d);
+  }
+}
+template <class S>
+static int hdiv_entry(int m, int n, const double* dA, const double* dB, void* W, int ldw, void* ws, size_t wsb,
+                      cudaStream_t st, int* info) {
+  if (!ws || wsb < sizeof(int)) return SYLV_EWORKSPACE;
+  int* fz = (int*)ws;
+  first_nonfinite_init_kernel<<<1, 1, 0, st>>>(fz);
+  MSY_LAUNCH_CK();
+  hdiv_kernel<S><<<dim3(cdiv(m, 256), std::min(n, 65535)), 256, 0, st>>>(m, n, dA, dB, (S*)W, ldw, fz);
+  MSY_LAUNCH_CK();
+  int h = 0;
+  MSY_CK(d2h(&h, fz, sizeof(int), st));
+  if (info) {
+    info[0] = h == 0x7fffffff ? SYLV_OK : SYLV_SINGULAR_EQUATION;
+    info[1] = h == 0x7fffffff ? -1 : h / n;
+    info[2] = h == 0x7fffffff ? -1 : h % n;
+  }
+  return 0;
+}
+int sylv_hdiv(int dtype, int m, int n, const double* dA, const double* dB, void* W, int ldw, void* ws,
+              size_t ws_bytes, void* stream, int* info) {
+  if ((dtype != 1 && dtype != 3) || m < 1 || n < 1 || ldw < m || !dA || !dB || !W) return SYLV_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == 1) return hdiv_entry<double>(m, n, dA, dB, W, ldw, ws, ws_bytes, st, info);
+  return hdiv_entry<cdouble>(m, n, dA, dB, W, ldw, ws, ws_bytes, st, info);
 }
 

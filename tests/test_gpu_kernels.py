@@ -247,3 +247,45 @@ def test_orth_cholesky_qr(B200, rng, m):
     assert np.linalg.norm(fc.Q @ fc.R - Uc) < 1e-13 * m
     assert (np.diag(fc.R).real > 0).all() and np.abs(np.diag(fc.R).imag).max() < 1e-15
 
+
+
+def test_hermitian_eig_reference_kats(B200, rng):
+    """pkg/tests/test_linalg.py:246-270: identity, [[2,1],[1,2]] -> {1, 3}, random Hermitian
+    reconstruction and unitarity, non-Hermitian input rejected."""
+    U, d = B200.hermitian_eig(np.eye(3))
+    assert np.allclose(np.sort(d), 1.0) and np.allclose(U.conj().T @ U, np.eye(3))
+    U, d = B200.hermitian_eig(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    assert np.allclose(np.sort(d), [1.0, 3.0], atol=1e-14)
+    for n in (9, 40, 150):
+        H = cmat(rng, n, n)
+        H = (H + H.conj().T) / 2
+        U, d = B200.hermitian_eig(H)
+        assert np.linalg.norm(U @ np.diag(d) @ U.conj().T - H) <= 100 * n * 2.0 ** -53 * np.linalg.norm(H)
+        assert np.linalg.norm(U.conj().T @ U - np.eye(n)) <= 100 * n * 2.0 ** -53
+        assert np.allclose(np.sort(d), np.linalg.eigvalsh(H), atol=1e-12 * np.abs(d).max())
+    from paper_2503_03456_b200.errors import NotHermitianError
+    with pytest.raises(NotHermitianError):
+        B200.hermitian_eig(cmat(rng, 4, 4))
+
+
+@pytest.mark.parametrize("m,n,cplx", [(7, 5, True), (60, 45, False), (300, 200, False)])
+def test_solve_hermitian_matches_kronecker(B200, rng, m, n, cplx):
+    """solve_hermitian (sylvester.py:181-196) against the explicit Kronecker solve
+    (pkg/tests/test_sylvester.py:150-165 and acceptance criterion 2, test_acceptance.py:85-115)."""
+    def herm(k, shift):
+        G = cmat(rng, k, k) if cplx else rng.standard_normal((k, k))
+        return (G + G.conj().T) / 2 + shift * np.eye(k)
+    A, B = herm(m, 3.0 + np.sqrt(m)), herm(n, 1.0 + np.sqrt(n))
+    C = cmat(rng, m, n) if cplx else rng.standard_normal((m, n))
+    p = B200.SylvesterProblem(A, B, C, kind="hermitian")
+    X = B200.solve_hermitian(p)
+    if m * n <= 4096:
+        Xk = np.linalg.solve(np.kron(np.eye(n), A) + np.kron(B.T, np.eye(m)), C.flatten("F")).reshape((m, n), order="F")
+        assert np.linalg.norm(X - Xk) <= 1e-11 * np.linalg.norm(Xk)
+    assert B200.residual(p, X) <= 1e-14
+    with pytest.raises(ValueError):
+        B200.solve_hermitian(B200.SylvesterProblem(A, B, C))
+    # exactly singular: spec(A) meets spec(-B)
+    with pytest.raises(B200.SingularEquationError):
+        B200.solve_hermitian(B200.SylvesterProblem(np.diag([1.0, 2.0]), np.diag([-2.0]), np.ones((2, 1)),
+                                                   kind="hermitian"))
