@@ -24,7 +24,7 @@ from .condition import _gemm
 from .errors import DimensionError, NotHermitianError, SingularEquationError, UnsupportedPrecisionError
 from .linalg import schur_tensor
 from .precision import format_bits
-from .sylvester import _is_real, as_matrix
+from .sylvester import as_matrix
 
 _U64 = 2.0 ** -53
 
@@ -35,8 +35,10 @@ def _check_ctx(ctx):
 
 
 def _eig_tensor(A: torch.Tensor):
-    """Column-major Hermitian device tensor -> (U, d) device tensors (d real float64)."""
-    T, U = schur_tensor(A.clone())
+    """Column-major Hermitian device tensor -> (U, d) device tensors (U complex128, d float64).
+    Always the complex Schur form: it is triangular (every 2x2 block split), so its diagonal
+    is the spectrum even where a real quasi-triangular form would keep a 2x2 block."""
+    T, U = schur_tensor(A.to(torch.complex128).clone())
     d = torch.diagonal(T).real.to(torch.float64).contiguous()
     return U, d
 
@@ -53,10 +55,8 @@ def hermitian_eig(A, ctx=None, dev=None):
         raise NotHermitianError("input is not Hermitian to working accuracy")
     if n == 1:
         return np.eye(1, dtype=np.complex128), np.array([A[0, 0].real])
-    real = _is_real(A)
     dev = D.device(dev)
-    t = D.to_cm(np.real(A) if real else A, torch.float64 if real else torch.complex128, dev)
-    U, d = _eig_tensor(t)
+    U, d = _eig_tensor(D.to_cm(A, torch.complex128, dev))
     return D.from_cm(U).astype(np.complex128), d.cpu().numpy()
 
 
@@ -71,10 +71,9 @@ def solve_hermitian(p, ctx=None, dev=None) -> np.ndarray:
         nrm = float(np.linalg.norm(M))
         if float(np.linalg.norm(M - M.conj().T)) > 10 * _U64 * max(nrm, 1e-300):
             raise NotHermitianError("input is not Hermitian to working accuracy")
-    real = _is_real(A, B, C)
-    dt = torch.float64 if real else torch.complex128
+    dt = torch.complex128  # the eigenvectors are complex (complex Schur); X is returned complex128
     dev = D.device(dev)
-    cv = (lambda M: D.to_cm(np.real(M) if real else M, dt, dev))
+    cv = (lambda M: D.to_cm(M, dt, dev))
     tA, tB, tC = cv(A), cv(B), cv(C)
     if m > 1:
         UA, dA = _eig_tensor(tA)
@@ -84,7 +83,7 @@ def solve_hermitian(p, ctx=None, dev=None) -> np.ndarray:
         UB, dB = _eig_tensor(tB)
     else:
         UB, dB = torch.ones((1, 1), dtype=dt, device=dev), tB.reshape(1).real.to(torch.float64)
-    adj = b"C" if tC.is_complex() else b"T"
+    adj = b"C"
     tmp = torch.empty_like(tC)
     Y = torch.empty_like(tC)
     _gemm(adj, b"N", UA, tC, tmp, 1.0, 0.0, m, n, m, m, m, m)     # U_A^H C

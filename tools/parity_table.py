@@ -39,7 +39,7 @@ for config in ("c0", "c1", "c2", "c3", "ch"):
             r["fwd_vs_Xtrue_ref"] = float(g["fwd_true"])
         if pr.kind == "lyapunov":
             r["asym"] = float(np.linalg.norm(X - X.T) / np.linalg.norm(X))
-        r["pass"] = (abs(r["k"] - r["k_ref"]) <= 1 and be <= 10 * max(be_ref, U64) and r["rel_diff_vs_ref"] <= r["bar"])
+        r["pass"] = bool(abs(r["k"] - r["k_ref"]) <= 1 and be <= 10 * max(be_ref, U64) and r["rel_diff_vs_ref"] <= r["bar"])
         rows.append(r)
         print(json.dumps(r), flush=True)
 with open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/parity.json", "w") as f:
