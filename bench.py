@@ -235,16 +235,25 @@ KPREFIX = {0: "gemm_dmma", 1: "gemm_simt", 2: "apply_z", 3: "chase", 4: "trsyl",
 
 
 def ncu_traffic(cls):
-    """Per-launch DRAM bytes of a kernel class from the newest committed `ncu --set full` capture
-    (profiles/*ncu_full_capture.json), or (None, None)."""
+    """Per-launch DRAM bytes (read + write) of a kernel class from the newest committed `ncu --set
+    full` summary (profiles/r*_ncu_full_kernels.json, or the older *ncu_full_capture.json), or
+    (None, None)."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full_capture.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full_*.json")), key=os.path.getmtime)
+    unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for f in reversed(files):
         try:
             with open(f) as fh:
                 cap = json.load(fh)
         except Exception:
             continue
+        for name, d in cap.get("kernels", {}).items():
+            if name.startswith(KPREFIX.get(cls, "?")):
+                tot = 0.0
+                for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, u = (d.get(key, "0 byte").split() + ["byte"])[:2]
+                    tot += float(v) * unit.get(u, 1.0)
+                return tot, f"{os.path.relpath(f, ROOT)}: {name}, one launch (grid {d.get('launch__grid_size')})"
         ls = [l for l in cap.get("launches", []) if l.get("kernel", "").startswith(KPREFIX.get(cls, "?"))]
         if ls:
             return (sum(l["dram_bytes"] for l in ls) / len(ls),

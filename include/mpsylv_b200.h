@@ -167,6 +167,25 @@ int sylv_gemm(int dtype, char opa, char opb, int m, int n, int k, const void* al
 int sylv_hdiv(int dtype, int m, int n, const double* dA, const double* dB, void* W, int ldw, void* ws,
               size_t ws_bytes, void* stream, int* info);
 
+/* mp_orth / mp_inv with the low-precision Schur factors supplied by the caller (the
+ * _low_precision_schur_pair step, refinement.py:190-197, done elsewhere -- e.g. Schur(B) on a
+ * second GPU): TA, UA (m x m) and TB, UB (n x n) in the low precision of `p` (float for real,
+ * complex64 for complex data when low_bits = 32), column-major.  Everything else as
+ * sylv_solve; the workspace is sylv_workspace_size's. */
+int sylv_solve_factored(const sylv_params* p, const void* A, int lda, const void* B, int ldb, const void* C, int ldc,
+                        void* X, int ldx, const void* TA, int ldta, const void* UA, int ldua, const void* TB, int ldtb,
+                        const void* UB, int ldub, void* ws, size_t ws_bytes, void* stream, sylv_report* report);
+
+/* GMRES-IR inner solver (gmresir.py:112-205), one Arnoldi step in one launch: modified
+ * Gram-Schmidt of w (N) against the columns 0..j of V (N x (j+2), column-major, ld ldv),
+ * h[0..j] = the coefficients <v_i, w>, h[j+1] = ||w||_2 (real part), V[:, j+1] = w / ||w||
+ * (unless 0 / non-finite); w is overwritten.  h: HOST array of j+2 scalars of the dtype
+ * (j + 2 <= 256), filled before return (the call synchronises the stream).  j = -1: only the
+ * norm (h[0]) and V[:, 0] = w / ||w||. */
+int sylv_krylov_workspace_size(int dtype, int N, int j, size_t* bytes);
+int sylv_krylov_mgs(int dtype, int N, void* V, int ldv, int j, void* w, void* h, void* ws, size_t ws_bytes,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

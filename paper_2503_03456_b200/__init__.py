@@ -25,6 +25,7 @@ from .sylvester import DirectSolveReport, SylvesterProblem, bartels_stewart, res
 from .linalg import QrFactors, SchurFactors, gemm, mgs_qr, schur
 from .condition import KappaEstimate, kappa_sylv, kappa_sylv_tensor
 from .hermitian import hermitian_eig, solve_hermitian
+from .split2 import mp_inv_split2, mp_orth_split2, solve_factored
 from .gmresir import GmresConfig, GmresIrReport, apply_preconditioner, gmres_ir_sylv
 
 __version__ = "0.1.0"

@@ -29,6 +29,7 @@ EXPORTS = (
     "sylv_workspace_size", "sylv_solve", "sylv_batched_workspace_size", "sylv_solve_batched",
     "sylv_refine_workspace_size", "sylv_refine", "sylv_schur_workspace_size", "sylv_schur",
     "sylv_trsyl_workspace_size", "sylv_trsyl", "sylv_orth_workspace_size", "sylv_orth", "sylv_gemm", "sylv_hdiv",
+    "sylv_krylov_workspace_size", "sylv_krylov_mgs", "sylv_solve_factored",
 )
 
 
@@ -92,6 +93,10 @@ def lib():
         L.sylv_orth.argtypes = [ip, ip, vp, ip, vp, ip, vp, ip, vp, sz, vp, ct.POINTER(ct.c_int)]
         L.sylv_gemm.argtypes = [ip, ct.c_char, ct.c_char, ip, ip, ip, vp, vp, ip, vp, ip, vp, vp, ip, vp]
         L.sylv_hdiv.argtypes = [ip, ip, ip, vp, vp, vp, ip, vp, sz, vp, ct.POINTER(ct.c_int)]
+        L.sylv_krylov_workspace_size.argtypes = [ip, ip, ip, ct.POINTER(sz)]
+        L.sylv_krylov_mgs.argtypes = [ip, ip, vp, ip, ip, vp, vp, vp, sz, vp]
+        L.sylv_solve_factored.argtypes = [ct.POINTER(Params), vp, ip, vp, ip, vp, ip, vp, ip, vp, ip, vp, ip, vp, ip,
+                                          vp, ip, vp, sz, vp, ct.POINTER(Report)]
         _lib = L
     return _lib
 

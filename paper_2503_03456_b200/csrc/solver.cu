@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "krylov.cuh"
 #include "gemm.cuh"
 #include "gemm_dmma.cuh"
 #include "lu.cuh"
@@ -51,6 +52,12 @@ struct StreamCtx {
 thread_local StreamCtx g_ctx;
 // batched lanes: one stream per lane, Schur(A) then Schur(B) (concurrency comes from the lanes)
 thread_local bool t_serial_lane = false;
+// low-precision Schur factors supplied by the caller (sylv_solve_factored), column-major
+struct GivenFactors {
+  const void *TA, *UA, *TB, *UB;
+  int ldta, ldua, ldtb, ldub;
+};
+thread_local const GivenFactors* t_given = nullptr;
 
 int ctx_init() {
   int dev;
@@ -421,7 +428,16 @@ int solve_impl(const sylv_params* p, const Hh* A, int lda, const Hh* B, int ldb,
     if (!r2) r2 = gemm<Hh>('N', 'N', n, n, n, Hh(1), w.tmpB, n, w.QB, n, Hh(0), w.SB, n, ss);
     return r2;
   };
-  rc = run_schur_pair<Hh, Ll>(m, n, p->kind, A, lda, B, ldb, w, st, ovf, &sa, &sb, b_beside ? &post_b : nullptr);
+  if (t_given != nullptr) {  // sylv_solve_factored: the low-precision Schur factors come from the caller
+    const GivenFactors& g = *t_given;
+    rc = copy2d<Ll>(m, m, (const Ll*)g.TA, g.ldta, w.TA, m, st);
+    if (!rc) rc = copy2d<Ll>(m, m, (const Ll*)g.UA, g.ldua, w.UA, m, st);
+    if (!rc) rc = copy2d<Ll>(n, n, (const Ll*)g.TB, g.ldtb, w.TB, n, st);
+    if (!rc) rc = copy2d<Ll>(n, n, (const Ll*)g.UB, g.ldub, w.UB, n, st);
+    if (!rc && b_beside) rc = post_b(st);
+  } else {
+    rc = run_schur_pair<Hh, Ll>(m, n, p->kind, A, lda, B, ldb, w, st, ovf, &sa, &sb, b_beside ? &post_b : nullptr);
+  }
   if (rc) return rc;
   rep->schur_sweeps_a = sa.sweeps;
   rep->schur_sweeps_b = sb.sweeps;
@@ -1240,5 +1256,51 @@ int sylv_hdiv(int dtype, int m, int n, const double* dA, const double* dB, void*
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == 1) return hdiv_entry<double>(m, n, dA, dB, W, ldw, ws, ws_bytes, st, info);
   return hdiv_entry<cdouble>(m, n, dA, dB, W, ldw, ws, ws_bytes, st, info);
+}
+
+// ---- GMRES-IR Arnoldi step (krylov.cuh) ---------------------------------------------
+template <class S>
+static int krylov_entry(int N, void* V, int ldv, int j, void* w, void* h_host, void* ws, size_t wsb, cudaStream_t st) {
+  const int G = krylov_grid<S>(N);
+  if (G <= 0) return SYLV_ECUDA;
+  Arena ar(ws, wsb);
+  S* part = ar.get<S>((size_t)2 * G);
+  S* hd = ar.get<S>((size_t)j + 2);
+  if (!ar.ok()) return SYLV_EWORKSPACE;
+  int rc = krylov_mgs<S>(N, (S*)V, ldv, j, (S*)w, hd, part, G, st);
+  if (rc) return rc;
+  MSY_CK(d2h(h_host, hd, sizeof(S) * (size_t)(j + 2), st));
+  return 0;
+}
+int sylv_krylov_workspace_size(int dtype, int N, int j, size_t* bytes) {
+  if (!valid_dtype(dtype) || N < 1 || j < -1 || !bytes) return SYLV_EINVAL;
+  const size_t es = dtype == 0 ? 4 : (dtype == 3 ? 16 : 8);
+  *bytes = es * (2 * 2 * 148 * 8 + (size_t)j + 2) + 1024;  // partials for up to 8 blocks/SM x 148 SMs, x2
+  return 0;
+}
+int sylv_krylov_mgs(int dtype, int N, void* V, int ldv, int j, void* w, void* h, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (!valid_dtype(dtype) || N < 1 || j < -1 || ldv < N || !V || !w || !h) return SYLV_EINVAL;
+  if ((size_t)(j + 2) * (dtype == 3 ? 16 : 8) > 4096) return SYLV_EINVAL;  // readback staging cap
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (dtype) {
+    case 0: return krylov_entry<float>(N, V, ldv, j, w, h, ws, ws_bytes, st);
+    case 1: return krylov_entry<double>(N, V, ldv, j, w, h, ws, ws_bytes, st);
+    case 2: return krylov_entry<cfloat>(N, V, ldv, j, w, h, ws, ws_bytes, st);
+    default: return krylov_entry<cdouble>(N, V, ldv, j, w, h, ws, ws_bytes, st);
+  }
+}
+
+// ---- solve with caller-supplied Schur factors (the 2-GPU split: Schur(B) on another GPU) ----
+int sylv_solve_factored(const sylv_params* p, const void* A, int lda, const void* B, int ldb, const void* C, int ldc,
+                        void* X, int ldx, const void* TA, int ldta, const void* UA, int ldua, const void* TB, int ldtb,
+                        const void* UB, int ldub, void* ws, size_t ws_bytes, void* stream, sylv_report* rep) {
+  if (!p || !TA || !UA || !TB || !UB || ldta < p->m || ldua < p->m || ldtb < p->n || ldub < p->n) return SYLV_EINVAL;
+  if (p->variant == SYLV_VARIANT_BS) return SYLV_EUNSUPPORTED;
+  GivenFactors g{TA, UA, TB, UB, ldta, ldua, ldtb, ldub};
+  t_given = &g;
+  const int rc = sylv_solve(p, A, lda, B, ldb, C, ldc, X, ldx, ws, ws_bytes, stream, rep);
+  t_given = nullptr;
+  return rc;
 }
 

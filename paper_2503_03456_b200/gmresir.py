@@ -158,25 +158,69 @@ def apply_preconditioner(W, sf_A, sf_B, ctx=None):
 
 
 # ---------------------------------------------------------------------------
+_NP = {torch.float32: np.float32, torch.float64: np.float64, torch.complex64: np.complex64,
+       torch.complex128: np.complex128}
+
+
+def _krylov(V, j, w, N):
+    """sylv_krylov_mgs: MGS of w against V[:, 0..j], h[j+1] = ||w||, V[:, j+1] = w / ||w||
+    (one cooperative launch; j = -1: norm and V[:, 0] only).  Returns h (numpy, j+2)."""
+    L = _native.lib()
+    code = D.dtype_code(w)
+    sz = ct.c_size_t()
+    _native.check(L.sylv_krylov_workspace_size(code, N, j, ct.byref(sz)), "krylov workspace")
+    ws = D.workspace(sz.value, w.device)
+    h = np.zeros(j + 2, dtype=_NP[w.dtype])
+    _native.check(L.sylv_krylov_mgs(code, N, V.data_ptr(), N, j, w.data_ptr(), h.ctypes.data, ws.data_ptr(),
+                                    sz.value, D.stream_ptr(w.device)), "sylv_krylov_mgs")
+    return h
+
+
+def _vnorm(x) -> float:
+    """||x||_2 of a device vector / matrix through the Krylov kernel (a scratch column)."""
+    v = x.reshape(-1)
+    scratch = torch.empty_like(v)
+    return float(np.real(_krylov(scratch, -1, v, v.numel())[0]))
+
+
+def _axpy(y, x, alpha):
+    """y <- y + alpha x for flattened device vectors (a K = 1 product through sylv_gemm)."""
+    yv, xv = y.reshape(-1), x.reshape(-1)
+    one = torch.ones((1, 1), dtype=y.dtype, device=y.device)
+    N = yv.numel()
+    al, be = _scalar(alpha, y.dtype), _scalar(1.0, y.dtype)
+    _native.check(_native.lib().sylv_gemm(D.dtype_code(yv), b"N", b"N", N, 1, 1, al.ctypes.data, xv.data_ptr(), N,
+                                          one.data_ptr(), 1, be.ctypes.data, yv.data_ptr(), N,
+                                          D.stream_ptr(y.device)), "sylv_gemm")
+    return y
+
+
 def _gmres_correction(matvec, rhs, gcfg: GmresConfig, unit_roundoff: float):
     """Restarted GMRES on the flattened preconditioned system (gmresir.py:112-205).
-    rhs: column-major device matrix; returns (E, inner_iterations, stagnated)."""
+    rhs: column-major device matrix; returns (E, inner_iterations, stagnated).
+    Every O(N) step runs on the device: the Arnoldi step (MGS + norm + normalisation) is one
+    sylv_krylov_mgs launch, the basis combination x += V y and the restart residual are
+    sylv_gemm products; only the (p+1) x p Hessenberg least-squares problem (Givens
+    rotations) runs on the host, as in the reference."""
     shape, dt = rhs.shape, rhs.dtype
     b = rhs.reshape(-1)  # column-major storage flattened = vec (column stacking)
     N = b.numel()
     x = torch.zeros_like(b)
-    beta0 = float(torch.linalg.vector_norm(b))
+    p = gcfg.restart
+    cx = dt.is_complex
+    Vb = torch.empty((p + 1, N), dtype=dt, device=b.device)  # column-major N x (p+1)
+    beta0 = float(np.real(_krylov(Vb, -1, b, N)[0]))
     if beta0 == 0.0:
         return x.reshape(shape), 0, False
     tol = max(gcfg.inner_tol, 4.0 * unit_roundoff)
     total_inner = 0
     stagnated = False
-    p = gcfg.restart
-    cx = dt.is_complex
-    Vb = torch.empty((p + 1, N), dtype=dt, device=b.device)
+    x_zero = True
     for _ in range(gcfg.max_restarts):
-        r = (b - matvec(x)) if bool(torch.any(x != 0)) else b.clone()
-        beta = float(torch.linalg.vector_norm(r))
+        r = b.clone()
+        if not x_zero:
+            _axpy(r, matvec(x), -1.0)
+        beta = float(np.real(_krylov(Vb, -1, r, N)[0]))  # also V[:, 0] = r / beta
         if not np.isfinite(beta):
             return x.reshape(shape), total_inner, True
         if beta <= tol * beta0:
@@ -186,22 +230,17 @@ def _gmres_correction(matvec, rhs, gcfg: GmresConfig, unit_roundoff: float):
         cs = np.zeros(p, dtype=np.complex128)
         sn = np.zeros(p, dtype=np.complex128)
         g = np.zeros(p + 1, dtype=np.complex128)
-        Vb[0] = r / beta
         g[0] = beta
         j = 0
         while j < p:
             w = matvec(Vb[j])
-            for i in range(j + 1):  # modified Gram-Schmidt, like the reference
-                h = complex(torch.vdot(Vb[i], w))
-                H[i, j] = h
-                w = w - (h if cx else h.real) * Vb[i]
-            hq = float(torch.linalg.vector_norm(w))
+            h = _krylov(Vb, j, w, N)  # MGS like the reference, then ||w|| and v_{j+1}
+            H[: j + 1, j] = h[: j + 1] if cx else np.real(h[: j + 1])
+            hq = float(np.real(h[j + 1]))
             H[j + 1, j] = hq
             total_inner += 1
             if not np.isfinite(hq):
                 return x.reshape(shape), total_inner, True
-            if hq != 0.0:
-                Vb[j + 1] = w / hq
             for i in range(j):
                 t = np.conj(cs[i]) * H[i, j] + np.conj(sn[i]) * H[i + 1, j]
                 H[i + 1, j] = cs[i] * H[i + 1, j] - sn[i] * H[i, j]
@@ -226,7 +265,11 @@ def _gmres_correction(matvec, rhs, gcfg: GmresConfig, unit_roundoff: float):
                 acc = acc - H[i, l] * y[l]
             y[i] = acc / H[i, i]
         coef = torch.as_tensor(y if cx else y.real, dtype=dt, device=b.device)
-        x = x + coef @ Vb[:j]
+        al, be = _scalar(1.0, dt), _scalar(1.0, dt)
+        _native.check(_native.lib().sylv_gemm(D.dtype_code(x), b"N", b"N", N, 1, j, al.ctypes.data, Vb.data_ptr(), N,
+                                              coef.data_ptr(), j, be.ctypes.data, x.data_ptr(), N,
+                                              D.stream_ptr(x.device)), "sylv_gemm")  # x += V[:, :j] y
+        x_zero = False
         final = abs(g[j])
         if final <= tol * beta0:
             break
@@ -243,9 +286,8 @@ def _device_residual(tA, tB, tC, tX) -> float:
     R = tC.clone()
     _gemm("N", tA, "N", tX, R, -1.0, 1.0)
     _gemm("N", tX, "N", tB, R, -1.0, 1.0)
-    nr = float(torch.linalg.vector_norm(R))
-    den = float(torch.linalg.vector_norm(tC)) + float(torch.linalg.vector_norm(tX)) * (
-        float(torch.linalg.vector_norm(tA)) + float(torch.linalg.vector_norm(tB)))
+    nr = _vnorm(R)
+    den = _vnorm(tC) + _vnorm(tX) * (_vnorm(tA) + _vnorm(tB))
     return 0.0 if den == 0.0 else nr / den
 
 
@@ -302,12 +344,13 @@ def gmres_ir_sylv(p, gcfg: GmresConfig, rcfg: RefinementConfig, counter: FlopCou
         except (SingularEquationError, NumericBreakdownError) as exc:
             failure = f"preconditioner failure: {exc}"
             break
-        X = X + E.to(dth)
+        Eh = E.to(dth)
+        _axpy(X, Eh, 1.0)
         outer += 1
         inner_counts.append(li)
         history.append(_device_residual(tA, tB, tC, X))
-        nE = float(torch.linalg.vector_norm(E.to(dth)))
-        nX = float(torch.linalg.vector_norm(X))
+        nE = _vnorm(Eh)
+        nX = _vnorm(X)
         if not (np.isfinite(nE) and np.isfinite(nX)):
             failure = "nan_breakdown: iterate diverged to non-finite values"
             break

@@ -107,3 +107,39 @@ def test_device_gmres_ir_larger(cfg, m, n, ug):
     assert rep.outer_iterations <= 4
     if pr.X_true is not None:
         assert np.linalg.norm(rep.X - pr.X_true) / np.linalg.norm(pr.X_true) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt", ["float64", "complex128", "float32"])
+def test_krylov_step_kernel_matches_mgs(dt):
+    """sylv_krylov_mgs (one cooperative launch) == modified Gram-Schmidt as in gmresir.py:131-140,
+    plus the norm and the normalised new basis vector; deterministic run to run."""
+    import torch
+    from paper_2503_03456_b200.gmresir import _krylov
+    tdt = getattr(torch, dt)
+    rng = np.random.default_rng(5)
+    N, j = 70001, 6
+    def rnd(*s):
+        a = rng.standard_normal(s) + (1j * rng.standard_normal(s) if "complex" in dt else 0)
+        return torch.as_tensor(a).to(tdt).cuda()
+    V = torch.empty((j + 2, N), dtype=tdt, device="cuda")
+    Q, _ = torch.linalg.qr(rnd(N, j + 1).cpu().to(torch.complex128 if "complex" in dt else torch.float64))
+    V[: j + 1] = Q.t().to(tdt).cuda()
+    w0 = rnd(N)
+    w = w0.clone()
+    h = _krylov(V, j, w, N)
+    # numpy MGS in float64 / complex128
+    wn = w0.cpu().numpy().astype(np.complex128)
+    Vn = V[: j + 1].cpu().numpy().astype(np.complex128)
+    hr = []
+    for i in range(j + 1):
+        hi = np.vdot(Vn[i], wn)
+        hr.append(hi)
+        wn = wn - hi * Vn[i]
+    tol = 1e-5 if dt == "float32" else 1e-12
+    assert np.allclose(h[: j + 1], hr, atol=tol * np.abs(hr).max())
+    assert abs(np.real(h[j + 1]) - np.linalg.norm(wn)) <= tol * np.linalg.norm(wn)
+    assert np.allclose(V[j + 1].cpu().numpy(), wn / np.linalg.norm(wn), atol=10 * tol)
+    w2 = w0.clone()
+    h2 = _krylov(V, j, w2, N)
+    assert np.array_equal(h, h2) and torch.equal(w, w2)

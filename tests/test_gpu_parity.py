@@ -182,3 +182,27 @@ def test_batched_c4_size_against_oracle(B200, oracle):
         assert abs(reps[i].iterations - ref["iterations"]) <= 1
         be_ref = backward(p.A, p.B, p.C, ref["X"].real)
         assert backward(p.A, p.B, p.C, X[i].cpu().numpy()) <= 10 * max(be_ref, U64)
+
+
+@pytest.mark.parametrize("config,m,n", [("c0", 300, 200), ("c3", 160, 160), ("c2", 700, 400)])
+def test_factored_solve_matches_oracle(B200, oracle, config, m, n):
+    """sylv_solve_factored (the 2-GPU split's second half) with Schur factors computed separately
+    (split2.solve_factored): same bars against the oracle as the fused solve."""
+    import torch
+    from paper_2503_03456_b200 import device as D, problems as P
+    from paper_2503_03456_b200.linalg import schur_tensor
+    from paper_2503_03456_b200.split2 import solve_factored
+    pr = P.make(config, m, n, seed=1)
+    cx = pr.is_complex
+    dth, dtl = (torch.complex128, torch.complex64) if cx else (torch.float64, torch.float32)
+    dev = D.device()
+    cv = (lambda M, dt: D.to_cm(M if cx else np.real(M), dt, dev))
+    TA, UA = schur_tensor(cv(pr.A, dtl))
+    TB, UB = schur_tensor(cv(pr.B, dtl))
+    for variant in ("orth", "inv"):
+        X, rep = solve_factored(cv(pr.A, dth), cv(pr.B, dth), cv(pr.C, dth), TA, UA, TB, UB, variant=variant)
+        assert rep.status == 0
+        ref = oracle.mp_solve(pr.A, pr.B, pr.C, variant, "binary32")
+        Xn = D.from_cm(X)
+        assert abs(rep.iterations - ref["iterations"]) <= 1
+        assert backward(pr.A, pr.B, pr.C, Xn) <= 10 * max(backward(pr.A, pr.B, pr.C, ref["X"]), U64)

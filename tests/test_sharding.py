@@ -82,3 +82,36 @@ def test_gather_solutions_gloo_world2(total):
     assert got.shape == (total, 3, 2)
     for i in range(total):
         assert (got[i] == i).all()
+
+
+def _split_worker(rank, world, port, q):
+    """The 2-GPU split's exchange (split2.exchange_b_factors) on gloo: rank 1 'factors' B (a
+    stand-in for the device Schur) and sends (T_B, U_B) to rank 0; the other ranks idle."""
+    from paper_2503_03456_b200.split2 import exchange_b_factors
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 5
+    B = torch.arange(n * n, dtype=torch.float32).reshape(n, n) if rank == 1 else None
+    got = exchange_b_factors(lambda Bm: (2 * Bm, Bm + 1), B, n, torch.float32, torch.device("cpu"), 0, 1)
+    if rank == 0:
+        q.put((got[0].numpy().copy(), got[1].numpy().copy()))
+    else:
+        assert got is None
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split2_exchange_gloo(world):
+    import numpy as np
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    TB, UB = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    B = np.arange(25, dtype=np.float32).reshape(5, 5)
+    assert np.array_equal(TB, 2 * B) and np.array_equal(UB, B + 1)
