@@ -67,6 +67,31 @@ def test_gemm_ops_tn_nt(B200, rng):
             assert rel(got, ref) < (1e-5 if code in (0, 2) else 1e-13)
 
 
+def test_gemm_complex128_dmma_all_ops(B200, rng):
+    """complex128 GEMMs run on the DMMA tensor pipe (gemm_zdmma_kernel): every op pair, complex
+    alpha / beta, ragged tile edges, against the numpy complex128 product."""
+    import torch
+    from paper_2503_03456_b200 import _native
+    m, n, k = 131, 70, 75
+    alpha = np.array([0.75 - 0.5j], np.complex128)
+    beta = np.array([-0.25 + 1.5j], np.complex128)
+    op = {b"N": lambda X: X, b"T": lambda X: X.T, b"C": lambda X: X.conj().T}
+    for opa in (b"N", b"T", b"C"):
+        for opb in (b"N", b"T", b"C"):
+            A = cmat(rng, m, k) if opa == b"N" else cmat(rng, k, m)
+            Bm = cmat(rng, k, n) if opb == b"N" else cmat(rng, n, k)
+            C0 = cmat(rng, m, n)
+            tA = torch.as_tensor(A.T.copy()).cuda()
+            tB = torch.as_tensor(Bm.T.copy()).cuda()
+            tC = torch.as_tensor(C0.T.copy()).cuda()
+            rc = _native.lib().sylv_gemm(3, opa, opb, m, n, k, alpha.ctypes.data, tA.data_ptr(), A.shape[0],
+                                         tB.data_ptr(), Bm.shape[0], beta.ctypes.data, tC.data_ptr(), m,
+                                         torch.cuda.current_stream().cuda_stream)
+            assert rc == 0
+            ref = alpha[0] * (op[opa](A) @ op[opb](Bm)) + beta[0] * C0
+            assert rel(tC.t().cpu().numpy(), ref) < 1e-14, (opa, opb)
+
+
 @pytest.mark.parametrize("name", ["binary32", "binary64"])
 def test_trsyl_matches_oracle_complex(B200, oracle, golden_kernels, name):
     from paper_2503_03456_b200 import BINARY32, BINARY64, PrecisionContext

@@ -12,4 +12,6 @@ A, B, C = (torch.as_tensor(x, device="cuda").to(dt) for x in (pr.A, pr.B, pr.C))
 for _ in range(reps):
     X, rep = M.solve(A, B, C, kind=pr.kind)
 torch.cuda.synchronize()
-print("status", rep.status, "k", rep.iterations, "total ms", rep.ms_total)
+print("status", rep.status, "k", rep.iterations, "total ms", rep.ms_total, "schur", rep.ms_schur, "orth", rep.ms_orth,
+      "setup", rep.ms_setup, "y0", rep.ms_y0, "refine", rep.ms_refine, "recover", rep.ms_recover,
+      "sweeps", rep.schur_sweeps_a, rep.schur_sweeps_b)
