@@ -57,3 +57,6 @@
 #ifndef MSY_LANE_HESS_CAP
 #define MSY_LANE_HESS_CAP 0    // cap on each batched lane's cooperative Hessenberg grid (0: none)
 #endif
+#ifndef MSY_FAR_MIN_TILES
+#define MSY_FAR_MIN_TILES 64   // single-job Z applications of at least this many 32-wide tiles use the far kernel (-1: far kernel off)
+#endif

@@ -397,6 +397,141 @@ __global__ void __cluster_dims__(Azc<S>::N, 1, 1) __launch_bounds__(AZC_THREADS)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Throughput-oriented Z application for the FAR regions of real fp32 sweeps (the parts of the
+// rows right of / columns above a window, and U, that the next chase does not wait for).
+// One CTA owns a 64-wide tile with the full nz-deep contraction (in place: the input tile is
+// staged in smem before any output is written), 256 threads with an 8 x 4 register tile each:
+// per contraction step two LDS.128 of the row-major Z copy and four scalar / one LDS.128 of
+// the input tile feed 32 FFMAs (the cluster kernel above: 3 loads per 8 FFMAs and a 4x
+// redundant input read -- it stays the low-latency path for the near regions).  Outputs go
+// through smem so that global stores are warp-contiguous.
+constexpr int AZF_THREADS = 256, AZF_TILE = 64, AZF_W = 128, AZF_LDZ = 132, AZF_LDT = 65, AZF_LDC = 68;
+constexpr int AZF_TS = 128 * 68;  // floats of the tile / output staging buffer (>= 64 * 132, 128 * 65, 128 * 68)
+static size_t azf_smem() { return (size_t)(AZF_W * AZF_LDZ + AZF_TS) * sizeof(float); }
+__global__ void __launch_bounds__(AZF_THREADS, 2)
+    apply_z_far_kernel(float* H, int ldh, float* U, int ldu, const ApplyJobs<float> jobs) {
+  extern __shared__ __align__(16) unsigned char azf_raw[];
+  float* Zs = (float*)azf_raw;         // Zs[k * LDZ + o] = Z[k, o], zero beyond nz
+  float* Ts = Zs + AZF_W * AZF_LDZ;
+  int b = blockIdx.x;
+  int j = 0;
+  while (j + 1 < jobs.n && b >= jobs.start[j + 1]) j++;
+  b -= jobs.start[j];
+  const int nz = jobs.nz[j], r0 = jobs.r0[j];
+  const float* __restrict__ Zg = jobs.Z[j];
+  const int cL0 = jobs.cL0[j], cL1 = jobs.cL1[j], rlo = jobs.rlo[j], rR1 = jobs.rR1[j], mU = jobs.mU[j];
+  const int ntL = cL1 > cL0 ? cdiv(cL1 - cL0, AZF_TILE) : 0, ntR = rR1 > rlo ? cdiv(rR1 - rlo, AZF_TILE) : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {  // Z, transposed on the way in: thread (k, 4 columns) -> one conflict-free STS.128
+    const int k = tid & 127;
+#pragma unroll 4
+    for (int it = 0; it < 16; it++) {
+      const int o = 4 * ((tid >> 7) + 2 * it);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < nz) {
+        if (o < nz) v.x = Zg[k + (size_t)o * nz];
+        if (o + 1 < nz) v.y = Zg[k + (size_t)(o + 1) * nz];
+        if (o + 2 < nz) v.z = Zg[k + (size_t)(o + 2) * nz];
+        if (o + 3 < nz) v.w = Zg[k + (size_t)(o + 3) * nz];
+      }
+      *reinterpret_cast<float4*>(&Zs[k * AZF_LDZ + o]) = v;
+    }
+  }
+  // warp -> (output half h, group of 16 tile columns / rows cq); lane -> (ig, cg)
+  const int h = warp & 1, cq = warp >> 1, ig = lane & 7, cg = lane >> 3;
+  const int oa = h * 64 + ig * 4, ob = oa + 32, tb = cq * 16 + cg * 4;
+  float acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; a++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) acc[a][q] = 0.f;
+  if (b < ntL) {  // ---- region L: H[r0 + o, c] <- sum_k Z[k, o] H[r0 + k, c] ----
+    const int c0 = cL0 + b * AZF_TILE, nc = min(AZF_TILE, cL1 - c0);
+    for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {  // lanes along k: coalesced, conflict-free
+      const int k = e & 127, c = e >> 7;
+      Ts[k * AZF_LDT + c] = (k < nz && c < nc) ? H[(r0 + k) + (size_t)(c0 + c) * ldh] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < nz; k++) {
+      const float4 za = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oa]);
+      const float4 zb = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + ob]);
+      const float z[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+      float t[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) t[q] = Ts[k * AZF_LDT + tb + q];
+#pragma unroll
+      for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[a][q] = fmaf(z[a], t[q], acc[a][q]);
+    }
+    __syncthreads();
+    // outputs staged as Os[c * LDZ + o] (o contiguous, like global memory)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      *reinterpret_cast<float4*>(&Ts[(tb + q) * AZF_LDZ + oa]) = make_float4(acc[0][q], acc[1][q], acc[2][q], acc[3][q]);
+      *reinterpret_cast<float4*>(&Ts[(tb + q) * AZF_LDZ + ob]) = make_float4(acc[4][q], acc[5][q], acc[6][q], acc[7][q]);
+    }
+    __syncthreads();
+    for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {
+      const int o = e & 127, c = e >> 7;
+      if (o < nz && c < nc) H[(r0 + o) + (size_t)(c0 + c) * ldh] = Ts[c * AZF_LDZ + o];
+    }
+    return;
+  }
+  b -= ntL;
+  float* M;
+  int ldm, rbase, nrows;
+  if (b < ntR) { M = H; ldm = ldh; rbase = rlo + b * AZF_TILE; nrows = min(AZF_TILE, rR1 - rbase); }
+  else { b -= ntR; M = U; ldm = ldu; rbase = b * AZF_TILE; nrows = min(AZF_TILE, mU - rbase); }
+  if (nrows <= 0) return;
+  // ---- regions R / U: M[r, r0 + o] <- sum_k M[r, r0 + k] Z[k, o] ----
+  for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {  // lanes along r: coalesced, contiguous smem
+    const int r = e & 63, k = e >> 6;
+    Ts[k * AZF_LDC + r] = (k < nz && r < nrows) ? M[(rbase + r) + (size_t)(r0 + k) * ldm] : 0.f;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int k = 0; k < nz; k++) {
+    const float4 za = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oa]);
+    const float4 zb = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + ob]);
+    const float z[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+    const float4 tv = *reinterpret_cast<const float4*>(&Ts[k * AZF_LDC + tb]);
+    const float t[4] = {tv.x, tv.y, tv.z, tv.w};
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) acc[a][q] = fmaf(t[q], z[a], acc[a][q]);
+  }
+  __syncthreads();
+  // outputs staged as Os[o * LDC + r] (r contiguous, like global memory)
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    const int o = a < 4 ? oa + a : ob + (a - 4);
+    *reinterpret_cast<float4*>(&Ts[o * AZF_LDC + tb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+  }
+  __syncthreads();
+  for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {
+    const int r = e & 63, o = e >> 6;
+    if (o < nz && r < nrows) M[(rbase + r) + (size_t)(r0 + o) * ldm] = Ts[o * AZF_LDC + r];
+  }
+}
+// launch for a job list whose `start` was built for 32-wide tiles: rebuilt here for 64-wide ones
+static int apply_z_far_launch(float* H, int ldh, float* U, int ldu, ApplyJobs<float> jb, cudaStream_t st) {
+  MSY_SMEM_ATTR_ONCE(apply_z_far_kernel, (int)azf_smem());
+  jb.start[0] = 0;
+  for (int j = 0; j < jb.n; j++)
+    jb.start[j + 1] = jb.start[j] + (jb.cL1[j] > jb.cL0[j] ? cdiv(jb.cL1[j] - jb.cL0[j], AZF_TILE) : 0) +
+                      (jb.rR1[j] > jb.rlo[j] ? cdiv(jb.rR1[j] - jb.rlo[j], AZF_TILE) : 0) + cdiv(jb.mU[j], AZF_TILE);
+  if (jb.start[jb.n] <= 0) return 0;
+  apply_z_far_kernel<<<jb.start[jb.n], AZF_THREADS, azf_smem(), st>>>(H, ldh, U, ldu, jb);
+  MSY_LAUNCH_CK();
+  return 0;
+}
+template <class S>
+constexpr bool kFarKernel = std::is_same<S, float>::value && MsCfg<S>::W <= AZF_W;
+
 template <class S>
 static size_t applyz_smem(int nz) {
   return ((size_t)(nz + 1) * nz + (size_t)(nz + 1) * 33 + 32 * (size_t)nz) * sizeof(S) + 64;
@@ -419,6 +554,9 @@ int apply_z_regions(int m, int nz, const S* Z, S* H, int ldh, S* U, int ldu, int
     j.n = 1; j.start[0] = 0; j.start[1] = nblk;
     j.nz[0] = nz; j.Z[0] = Z; j.r0[0] = w0; j.cL0[0] = cL0; j.cL1[0] = cL1; j.rlo[0] = 0; j.rR1[0] = rR1;
     j.mU[0] = U ? m : 0;
+    if constexpr (kFarKernel<S>) {
+      if (MSY_FAR_MIN_TILES >= 0 && nblk >= MSY_FAR_MIN_TILES && nz >= 64) return apply_z_far_launch(H, ldh, U, ldu, j, st);
+    }
     apply_z_cl_kernel<S><<<nblk * Azc<S>::N, AZC_THREADS, azc_smem<S>(), st>>>(H, ldh, U, ldu, j);
   } else {
     apply_z_kernel<S><<<nblk, 256, applyz_smem<S>(nz), st>>>(nz, Z, H, ldh, w0, cL0, cL1, rR1, U, ldu, U ? m : 0);

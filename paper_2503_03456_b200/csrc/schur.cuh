@@ -13,17 +13,31 @@
 #include "schur_small.cuh"
 #include "schur_mss.cuh"
 #include "aed.cuh"
+#include "util.cuh"
 
 #include <chrono>
+#include <condition_variable>
 #include <cstdlib>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 namespace msy {
 
+#ifndef MSY_SUBMAX
+#define MSY_SUBMAX 640  // detached blocks up to this order are factored beside the sweeps (0: off)
+#endif
+#ifndef MSY_SUB_HELPERS
+#define MSY_SUB_HELPERS 3
+#endif
+constexpr int SUB_NH = MSY_SUB_HELPERS;  // helper host threads (and block workspaces) per Schur factorisation
+
+// workspace of one QR loop (deflation scan, shifts, sweeps, endgame blocks)
 template <class S>
-struct SchurWs {
+struct SchurLoopWs {
   typedef typename tr<S>::R R;
-  HessWs<S> hw;
   S* Z;       // 2 x ZMAX^2: window factors, double-buffered across overlapping windows
   S* sblk;    // trailing block copy
   R* wr;
@@ -33,8 +47,7 @@ struct SchurWs {
   S* vaed;    // AED window Schur vectors
   S* Zend;    // Schur vectors of the endgame blocks (sum of block orders^2 <= NMAX * m)
   int* dend;  // their [status, sweeps] words
-  static void carve(Arena& ar, int m, SchurWs& w) {
-    if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
+  static void carve(Arena& ar, int m, SchurLoopWs& w) {
     w.Z = ar.get<S>((size_t)2 * KMAX * ZMAX * ZMAX);
     w.sblk = ar.get<S>((size_t)EigCfg<S>::NMAX * EigCfg<S>::NMAX);
     w.wr = ar.get<R>(256);
@@ -44,6 +57,30 @@ struct SchurWs {
     w.vaed = m > SmallCfg<S>::NMAX ? ar.get<S>((size_t)AedCfg<S>::NW * AedCfg<S>::NW) : nullptr;
     w.Zend = m > SmallCfg<S>::NMAX ? ar.get<S>((size_t)SmallCfg<S>::NMAX * (m + SmallCfg<S>::NMAX)) : nullptr;
     w.dend = m > SmallCfg<S>::NMAX ? ar.get<int>(2 * (size_t)(m + 1)) : nullptr;
+  }
+};
+
+// Detached mid-size blocks (NMAX < order <= MSY_SUBMAX) are factored in place by a helper host
+// thread beside the sweeps of the remaining matrix (schur_device): `sub` is that QR loop's own
+// workspace, Zsub holds the blocks' Schur vectors (sum of orders^2 <= SUBMAX * m) and subtmp
+// the out-of-place product of one block's Z with its H rows / U columns.
+template <class S>
+struct SchurWs : SchurLoopWs<S> {
+  HessWs<S> hw;
+  SchurLoopWs<S> sub[SUB_NH];
+  S* Zsub = nullptr;
+  S* subtmp[SUB_NH] = {};
+  static void carve(Arena& ar, int m, SchurWs& w) {
+    if (m > SmallCfg<S>::NMAX) HessWs<S>::carve(ar, m, w.hw);
+    SchurLoopWs<S>::carve(ar, m, w);
+    w.Zsub = nullptr;
+    if (MSY_SUBMAX > SmallCfg<S>::NMAX && m > MSY_SUBMAX) {
+      w.Zsub = ar.get<S>((size_t)MSY_SUBMAX * m);
+      for (int i = 0; i < SUB_NH; i++) {
+        SchurLoopWs<S>::carve(ar, MSY_SUBMAX, w.sub[i]);
+        w.subtmp[i] = ar.get<S>((size_t)MSY_SUBMAX * m);
+      }
+    }
   }
 };
 
@@ -73,15 +110,80 @@ struct PhaseTimer {
 // auxiliary stream + events used to overlap the window chases (one CTA) with the
 // off-window Z applications (many CTAs).  Owned by a solve lane (solver.cu) or,
 // for direct sylv_schur calls, by the calling host thread.
+// Persistent helper host threads of one Schur factorisation: they run the QR loops of detached
+// mid-size blocks (shared FIFO), each on its own stream, while the owner keeps sweeping the rest.
+struct SubHelper {
+  static constexpr int NH = SUB_NH;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<std::function<void(int)>> q;
+  int pending = 0;
+  cudaStream_t st[NH] = {};
+  cudaEvent_t ev1[NH] = {};
+  std::vector<cudaEvent_t> evpool;  // one "block detached" event per job of the current loop
+  explicit SubHelper(int dev) {
+    int lo_pri = 0, hi_pri = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+    for (int i = 0; i < NH; i++) {
+      cudaStreamCreateWithPriority(&st[i], cudaStreamNonBlocking, (lo_pri + hi_pri) / 2);
+      cudaEventCreateWithFlags(&ev1[i], cudaEventDisableTiming);
+      std::thread([this, dev, i]() {
+        cudaSetDevice(dev);
+        for (;;) {
+          std::function<void(int)> j;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [this] { return !q.empty(); });
+            j = std::move(q.front());
+            q.pop_front();
+          }
+          j(i);
+          {
+            std::lock_guard<std::mutex> lk(mu);
+            pending--;
+          }
+          cv.notify_all();
+        }
+      }).detach();  // process lifetime, like the pair's side worker
+    }
+  }
+  cudaEvent_t job_event(size_t k) {  // owner thread only
+    while (evpool.size() <= k) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      evpool.push_back(e);
+    }
+    return evpool[k];
+  }
+  void push(std::function<void(int)> j) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      q.push_back(std::move(j));
+      pending++;
+    }
+    cv.notify_all();
+  }
+  void drain() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return pending == 0; });
+  }
+};
+
 struct SweepCtx {
   cudaStream_t aux = nullptr;  // nullptr: serial mode (everything on the caller's stream)
   cudaStream_t eg = nullptr;   // endgame blocks (one-CTA Schur + row-side Z), beside the sweeps
   cudaEvent_t evC = nullptr, evN = nullptr, evD = nullptr, evE0 = nullptr, evE1 = nullptr;
   int dev = -1;
+  SubHelper* helper = nullptr;  // created on first use (never for serial lanes)
+  SubHelper* sub_helper() {
+    if (!helper) helper = new SubHelper(dev);
+    return helper;
+  }
   void ensure() {
     int d = 0;
     cudaGetDevice(&d);
     if (aux != nullptr && dev == d) return;
+    helper = nullptr;  // a helper of another device keeps its own stream
     cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&eg, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&evC, cudaEventDisableTiming);
@@ -227,6 +329,13 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
           const ApplyJobs<S>& jb = rc_ == 0 ? jr[f] : jc[f];
           if (jb.start[nj] <= 0) continue;
           KScope ks(KC_APPLYZ, applyz_flops<S>(jb), s2);
+          if constexpr (kFarKernel<S>) {
+            if (f == 1 && MSY_FAR_MIN_TILES >= 0) {  // far parts: the throughput kernel
+              int rcf = apply_z_far_launch(H, ldh, U, ldu, jb, s2);
+              if (rcf) return rcf;
+              continue;
+            }
+          }
           if (cl)
             apply_z_cl_kernel<S><<<jb.start[nj] * Azc<S>::N, AZC_THREADS, azc_smem<S>(), s2>>>(H, ldh, U, ldu, jb);
           else
@@ -289,31 +398,49 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
   return 0;
 }
 
-// In place: A (m x m, lda) -> T; U (m x m, ldu) = Schur vectors.
+// Detached blocks handed to the helper thread: where they sit, where their Schur vectors are,
+// and what their QR loop reported.
+struct SubBlock { int lo, sz; size_t zoff; int rc, status, sweeps; };
 template <class S>
-int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_t st, SchurStats* stats,
-                 SweepCtx* sc = nullptr) {
-  if (!sc) sc = sweep_ctx();
+struct SubPlan {  // set for the top-level loop of a matrix that can spawn block jobs
+  SchurLoopWs<S>* ws;  // [SubHelper::NH]
+  S* Zsub;
+  S* const* tmp;       // [SubHelper::NH]
+};
+
+// C <- op(Z) C (left = true: rows x cols block C, Z rows x rows applied as Z^H) or C <- C Z
+// (left = false: Z cols x cols) through the out-of-place buffer tmp.
+template <class S>
+int apply_block_z(bool left, int rows, int cols, const S* Z, int ldz, S* C, int ldc, S* tmp, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return 0;
+  int rc = left ? gemm<S>('C', 'N', rows, cols, rows, S(1), Z, ldz, C, ldc, S(0), tmp, rows, st)
+                : gemm<S>('N', 'N', rows, cols, cols, S(1), C, ldc, Z, ldz, S(0), tmp, rows, st);
+  if (rc) return rc;
+  return copy2d<S>(rows, cols, tmp, rows, C, ldc, st);
+}
+
+// The QR iteration on an upper Hessenberg matrix, in place: A (m x m, lda) -> T, U (m x m, ldu)
+// <- U * (accumulated transformations).  `plan` (top level only) lets detached mid-size blocks
+// run on the helper thread.
+template <class S>
+int schur_qr_loop(int m, S* A, int lda, S* U, int ldu, SchurLoopWs<S>& w, cudaStream_t st, SchurStats& loc,
+                  SweepCtx* sc, PhaseTimer& pt, const SubPlan<S>* plan) {
   typedef typename tr<S>::R R;
   constexpr int NMIN = SmallCfg<S>::NMAX;
-  SchurStats loc = {};
-  if (m <= NMIN) {
-    int rc = schur_small_launch<S>(m, A, lda, U, ldu, SS_HESS | SS_WANTZ, nullptr, nullptr, w.dinfo, st);
-    if (rc) return rc;
-    int hinfo[2];
-    MSY_CK(d2h(hinfo, w.dinfo, sizeof(hinfo), st));
-    MSY_CK(host_sync(st));
-    loc.status = hinfo[0];
-    loc.sweeps = hinfo[1];
-    loc.small_calls = 1;
-    if (stats) *stats = loc;
-    return 0;
-  }
-  PhaseTimer pt(st);
-  int rc = hessenberg_blocked<S>(m, A, lda, U, ldu, w.hw, st);
-  if (rc) return rc;
-  pt.lap(&loc.ms_hess);
+  int rc = 0;
   int hi = m - 1, stag = 0, last_hi = m;
+  std::vector<SubBlock> subs;
+  subs.reserve(256);  // jobs hold pointers into it: never reallocated while they run (<= m / NMIN entries)
+  size_t zsoff = 0;
+  const bool sub_ok = plan != nullptr && plan->Zsub != nullptr && sc->aux != nullptr && MSY_SUBMAX > NMIN;
+  SubHelper* helper = nullptr;
+  int dev = 0;
+  if (sub_ok) cudaGetDevice(&dev);
+  const bool blocking = host_sync_blocking();
+  struct DrainGuard {  // jobs reference this frame: never leave it with jobs in flight
+    SubHelper*& h;
+    ~DrainGuard() { if (h) h->drain(); }
+  } drain_guard{helper};
   const int limit = 30 * m;
   // Endgame blocks (order <= NMAX split off below the active block) are solved beside the
   // sweeps on the endgame stream: their one-CTA Schur, the row-side Z (H rows of the block,
@@ -337,6 +464,44 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     if (hi < 0) break;
     if (hi < last_hi) { stag = 0; last_hi = hi; } else stag++;
     int sz = hi - lo + 1;
+    if (sub_ok && sz > NMIN && sz <= MSY_SUBMAX && subs.size() < 256 &&
+        zsoff + (size_t)sz * sz <= (size_t)MSY_SUBMAX * m) {
+      // detached block: its QR loop, the row side of its Z and U run on the helper's stream;
+      // the column side (rows above the block) is deferred to the end like the endgame blocks'
+      if (!helper) helper = sc->sub_helper();
+      cudaEvent_t evj = helper->job_event(subs.size());
+      MSY_CK(cudaEventRecord(evj, st));
+      subs.push_back({lo, sz, zsoff, 0, 0, 0});
+      SubBlock* sb = &subs.back();
+      zsoff += (size_t)sz * sz;
+      SubHelper* hp = helper;
+      const SubPlan<S> pl = *plan;
+      helper->push([=](int hidx) {
+        host_sync_blocking() = blocking;
+        cudaStream_t hs = hp->st[hidx];
+        cudaStreamWaitEvent(hs, evj, 0);
+        S* blk = A + sb->lo + (size_t)sb->lo * lda;
+        S* Zb = pl.Zsub + sb->zoff;
+        const int bs = sb->sz, b0 = sb->lo;
+        set_identity_kernel<S><<<dim3(cdiv(bs, 256), bs), 256, 0, hs>>>(bs, bs, Zb, bs);
+        __atomic_add_fetch(&launch_counter(), 1ULL, __ATOMIC_RELAXED);
+        SchurStats ls = {};
+        PhaseTimer pt2(hs);
+        pt2.on = false;
+        int r = schur_qr_loop<S>(bs, blk, lda, Zb, bs, pl.ws[hidx], hs, ls, sweep_ctx(), pt2, nullptr);
+        if (!r) r = apply_block_z<S>(true, bs, m - b0 - bs, Zb, bs, A + b0 + (size_t)(b0 + bs) * lda, lda, pl.tmp[hidx], hs);
+        if (!r) r = apply_block_z<S>(false, m, bs, Zb, bs, U + (size_t)b0 * ldu, ldu, pl.tmp[hidx], hs);
+        sb->rc = r;
+        sb->status = ls.status;
+        sb->sweeps = ls.sweeps;
+      });
+      loc.small_calls++;
+      hi = lo - 1;
+      last_hi = hi + 1;
+      stag = 0;
+      if (hi < 0) break;
+      continue;
+    }
     if (sz <= NMIN && async_end) {
       S* blk = A + lo + (size_t)lo * lda;
       S* Zb = w.Zend + zoff;
@@ -455,9 +620,14 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
                                             w.dinfo + 24);
     MSY_LAUNCH_CK();
     pt.lap(&loc.ms_shift);
+    const double sw0 = loc.ms_sweep;
+    const int nw0 = loc.windows;
     rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, K, w.shifts, w.Z, st, &loc.windows, sc);
     if (rc) return rc;
     pt.lap(&loc.ms_sweep);
+    if (pt.on && getenv("MSY_SCHUR_TRACE"))
+      fprintf(stderr, "sweep %d lo %d hi %d sz %d nb %d K %d wins %d ms %.3f\n", loc.ms_sweeps, lo, hi, sz, nb, K,
+              loc.windows - nw0, loc.ms_sweep - sw0);
     loc.sweeps++;
     loc.ms_sweeps++;
   }
@@ -481,8 +651,51 @@ int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_
     }
     pt.lap(&loc.ms_small);
   }
-  if (stats) *stats = loc;
+  if (helper) {  // join the helper, then the deferred column sides of its blocks
+    helper->drain();
+    for (int i = 0; i < SubHelper::NH; i++) {
+      MSY_CK(cudaEventRecord(helper->ev1[i], helper->st[i]));
+      MSY_CK(cudaStreamWaitEvent(st, helper->ev1[i], 0));
+    }
+    for (const SubBlock& b : subs) {
+      if (b.rc) return b.rc;
+      loc.sweeps += b.sweeps;
+      if (b.status && !loc.status) loc.status = b.status;
+      rc = apply_block_z<S>(false, b.lo, b.sz, plan->Zsub + b.zoff, b.sz, A + (size_t)b.lo * lda, lda, plan->tmp[0], st);
+      if (rc) return rc;
+    }
+    pt.lap(&loc.ms_small);
+  }
   return 0;
+}
+
+// In place: A (m x m, lda) -> T; U (m x m, ldu) = Schur vectors.
+template <class S>
+int schur_device(int m, S* A, int lda, S* U, int ldu, SchurWs<S>& w, cudaStream_t st, SchurStats* stats,
+                 SweepCtx* sc = nullptr) {
+  if (!sc) sc = sweep_ctx();
+  constexpr int NMIN = SmallCfg<S>::NMAX;
+  SchurStats loc = {};
+  if (m <= NMIN) {
+    int rc = schur_small_launch<S>(m, A, lda, U, ldu, SS_HESS | SS_WANTZ, nullptr, nullptr, w.dinfo, st);
+    if (rc) return rc;
+    int hinfo[2];
+    MSY_CK(d2h(hinfo, w.dinfo, sizeof(hinfo), st));
+    MSY_CK(host_sync(st));
+    loc.status = hinfo[0];
+    loc.sweeps = hinfo[1];
+    loc.small_calls = 1;
+    if (stats) *stats = loc;
+    return 0;
+  }
+  PhaseTimer pt(st);
+  int rc = hessenberg_blocked<S>(m, A, lda, U, ldu, w.hw, st);
+  if (rc) return rc;
+  pt.lap(&loc.ms_hess);
+  SubPlan<S> plan = {w.sub, w.Zsub, w.subtmp};
+  rc = schur_qr_loop<S>(m, A, lda, U, ldu, w, st, loc, sc, pt, &plan);
+  if (stats) *stats = loc;
+  return rc;
 }
 
 }  // namespace msy

@@ -371,6 +371,10 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
   side_worker().wait();  // always joined before job_b's captures go out of scope
   if (rc) return rc;
   if (rcb) return rcb;
+  if (getenv("MSY_SCHUR_TIMING"))  // diagnostic only (the phase timer synchronises at every lap)
+    for (const SchurStats* s : {sa, sb})
+      fprintf(stderr, "pair schur: hess %.1f ms, scan %.1f, small %.1f, shift %.1f, sweep %.1f | qr sweeps %d\n",
+              s->ms_hess, s->ms_scan, s->ms_small, s->ms_shift, s->ms_sweep, s->ms_sweeps);
   MSY_CK(cudaEventRecord(g_ctx.ev_a, sa_st));
   MSY_CK(cudaStreamWaitEvent(st, g_ctx.ev_a, 0));
   MSY_CK(cudaEventRecord(g_ctx.ev_side, side));
