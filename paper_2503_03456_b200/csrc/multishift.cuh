@@ -46,7 +46,10 @@ constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
 // rows/columns; the two phases order the only overlapping entries.  The warp
 // ops are branch-free (warp_left3 / warp_right3 redirect idle lanes to a dummy
 // row/column of the smem window).
-constexpr int KMAX = 8;  // bulge chains in flight per sweep (one CTA each)
+#ifndef MSY_KMAX
+#define MSY_KMAX 8
+#endif
+constexpr int KMAX = MSY_KMAX;  // bulge chains in flight per sweep (one CTA each)
 // fixed-trip, loads-first warp ops (wl3u / wr3u2) for real fp32 windows; the wider types keep
 // the loop forms (the unrolled register arrays would spill)
 template <class S> constexpr bool kFixedTrip = std::is_same<S, float>::value;
@@ -157,6 +160,212 @@ __global__ void __launch_bounds__(512) chase_kernel(S* H, int ldh, int lo, int h
 #undef HW
 #undef ZW
 }
+
+// ---------------------------------------------------------------------------
+// fp32 window chase on a CTA pair (thread-block cluster of 2).  The accumulated factor Z never
+// feeds back into the chase, so it moves to the partner CTA: rank 0 keeps the H window and, per
+// step, posts each bulge's reflector into the partner's shared memory (DSMEM) and raises a step
+// counter there; rank 1 replays the reflectors onto its Z (rows contiguous, one float4 per lane
+// covers the 128 rows of a column) one step behind.  The chaser sheds a third of its
+// shared-memory traffic and instructions, the pair finishes when the last step is replayed.
+#ifndef MSY_CHASE2
+#define MSY_CHASE2 1
+#endif
+constexpr int CZ_LD = 132, CZ_W = 128, CZ_NB = 16, CZ_THREADS = 32 * (CZ_NB + 1);
+constexpr int CZ_STEPS = CZ_W + 4 * CZ_NB;  // a window holds at most W + 4 (nb - 1) steps (the last one of a sweep)
+struct __align__(16) ChaseRec { float tau, v1, v2; int nr; };
+static size_t chase2_smem() {
+  const size_t a = (size_t)(CZ_W + 1) * CZ_W * sizeof(float);
+  const size_t b = (size_t)CZ_W * CZ_LD * sizeof(float) + (size_t)CZ_STEPS * CZ_NB * sizeof(ChaseRec) + 16;
+  return a > b ? a : b;
+}
+// H-only right application (rows 0..rH of columns c0..c0+2), fixed trip, loads first
+template <int LD, int NI>
+__device__ __forceinline__ void wr3h(float* H, int rH, int c0, float tau, float v1, float v2, int lane) {
+  float* ph = H + c0 * LD + lane;
+  float a0[NI], a1[NI], a2[NI];
+#pragma unroll
+  for (int k = 0; k < NI; k++)
+    if (lane + 32 * k <= rH) { a0[k] = ph[32 * k]; a1[k] = ph[32 * k + LD]; a2[k] = ph[32 * k + 2 * LD]; }
+#pragma unroll
+  for (int k = 0; k < NI; k++)
+    if (lane + 32 * k <= rH) {
+      const float w = tau * fmaf(a2[k], v2, fmaf(a1[k], v1, a0[k]));
+      ph[32 * k] = a0[k] - w;
+      ph[32 * k + LD] = a1[k] - w * v1;
+      ph[32 * k + 2 * LD] = a2[k] - w * v2;
+    }
+}
+template <int LD, int NI>
+__device__ __forceinline__ void wr2h(float* H, int rH, int c0, float tau, float v1, int lane) {
+  float* ph = H + c0 * LD + lane;
+  float a0[NI], a1[NI];
+#pragma unroll
+  for (int k = 0; k < NI; k++)
+    if (lane + 32 * k <= rH) { a0[k] = ph[32 * k]; a1[k] = ph[32 * k + LD]; }
+#pragma unroll
+  for (int k = 0; k < NI; k++)
+    if (lane + 32 * k <= rH) {
+      const float w = tau * fmaf(a1[k], v1, a0[k]);
+      ph[32 * k] = a0[k] - w;
+      ph[32 * k + LD] = a1[k] - w * v1;
+    }
+}
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CZ_THREADS)
+    chase2_kernel(float* H, int ldh, int lo, int hi, int nb, const ChaseJobs<float> jobs) {
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int rank = (int)cl.block_rank(), job = blockIdx.x >> 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ws = jobs.ws[job], we = jobs.we[job], t0 = jobs.t0[job], t1 = jobs.t1[job];
+  const int nw = we - ws;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // partner-side layout (rank 1's shared memory; rank 0 only forms remote addresses from it)
+  float* Zw = (float*)smem_raw;                                       // CZ_W columns, stride CZ_LD
+  ChaseRec* recs = (ChaseRec*)(Zw + CZ_W * CZ_LD);                    // [step][bulge]
+  int* flag = (int*)(recs + CZ_STEPS * CZ_NB);                            // steps posted so far
+  if (rank == 1) {
+    for (int e = tid; e < CZ_W * CZ_LD; e += CZ_THREADS) {
+      const int i = e % CZ_LD, jj = e / CZ_LD;
+      Zw[e] = (i == jj) ? 1.f : 0.f;
+    }
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    cl.sync();
+    const int j = warp;
+    for (int t = t0; t < t1; t++) {
+      if (tid == 0) {
+        volatile int* f = flag;
+        while (*f < t - t0 + 1) {}
+        __threadfence();
+      }
+      __syncthreads();
+      if (j < nb) {
+        const ChaseRec r = recs[(t - t0) * CZ_NB + j];
+        if (r.tau != 0.f) {
+          const int pl = lo - 1 + t - 4 * j - ws;
+          const int zmax = min(nw - 1, (lo - 1 + t) - ws + 3);
+          if (4 * lane <= zmax) {  // rows beyond zmax hold zeros in these columns: left as they are
+            float* pz = Zw + (pl + 1) * CZ_LD + 4 * lane;
+            const float4 z0 = *reinterpret_cast<const float4*>(pz);
+            const float4 z1 = *reinterpret_cast<const float4*>(pz + CZ_LD);
+            if (r.nr == 3) {
+              const float4 z2 = *reinterpret_cast<const float4*>(pz + 2 * CZ_LD);
+              float4 w;
+              w.x = r.tau * fmaf(z2.x, r.v2, fmaf(z1.x, r.v1, z0.x));
+              w.y = r.tau * fmaf(z2.y, r.v2, fmaf(z1.y, r.v1, z0.y));
+              w.z = r.tau * fmaf(z2.z, r.v2, fmaf(z1.z, r.v1, z0.z));
+              w.w = r.tau * fmaf(z2.w, r.v2, fmaf(z1.w, r.v1, z0.w));
+              *reinterpret_cast<float4*>(pz) = make_float4(z0.x - w.x, z0.y - w.y, z0.z - w.z, z0.w - w.w);
+              *reinterpret_cast<float4*>(pz + CZ_LD) =
+                  make_float4(z1.x - w.x * r.v1, z1.y - w.y * r.v1, z1.z - w.z * r.v1, z1.w - w.w * r.v1);
+              *reinterpret_cast<float4*>(pz + 2 * CZ_LD) =
+                  make_float4(z2.x - w.x * r.v2, z2.y - w.y * r.v2, z2.z - w.z * r.v2, z2.w - w.w * r.v2);
+            } else {
+              float4 w;
+              w.x = r.tau * fmaf(z1.x, r.v1, z0.x);
+              w.y = r.tau * fmaf(z1.y, r.v1, z0.y);
+              w.z = r.tau * fmaf(z1.z, r.v1, z0.z);
+              w.w = r.tau * fmaf(z1.w, r.v1, z0.w);
+              *reinterpret_cast<float4*>(pz) = make_float4(z0.x - w.x, z0.y - w.y, z0.z - w.z, z0.w - w.w);
+              *reinterpret_cast<float4*>(pz + CZ_LD) =
+                  make_float4(z1.x - w.x * r.v1, z1.y - w.y * r.v1, z1.z - w.z * r.v1, z1.w - w.w * r.v1);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    float* Zg = jobs.Z[job];
+    for (int e = tid; e < nw * nw; e += CZ_THREADS) {
+      const int i = e % nw, jj = e / nw;
+      Zg[i + (size_t)jj * nw] = Zw[i + jj * CZ_LD];
+    }
+    return;
+  }
+  // ---- rank 0: the chase proper (H window only) ----
+  const float* __restrict__ shifts = jobs.shifts[job];
+  constexpr int ld = CZ_W + 1;
+  float* Hw = (float*)smem_raw;
+#define HW(i, j) Hw[(i) + (j) * ld]
+  if (tid < 4 * CZ_W) {  // thread (row i, column class jc): 32 loads in flight
+    const int i = tid % CZ_W, jc = tid / CZ_W;
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const int jj = jc + 4 * k;
+      v[k] = (i < nw && jj < nw) ? H[(ws + i) + (size_t)(ws + jj) * ldh] : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const int jj = jc + 4 * k;
+      if (i < nw && jj < nw) HW(i, jj) = v[k];
+    }
+  }
+  ChaseRec* recs_r = cl.map_shared_rank(recs, 1);
+  int* flag_r = cl.map_shared_rank(flag, 1);
+  __syncthreads();
+  cl.sync();  // the partner runs and has cleared its step counter
+  const int j = warp;  // bulge handled by this warp (warp CZ_NB: the signalling warp)
+  constexpr int NI = CZ_W / 32;
+  for (int t = t0; t < t1; t++) {
+    const int p = lo - 1 + t - 4 * j;
+    const bool act = (j < nb) && (p >= lo - 1) && (p <= hi - 2);
+    float tau = 0.f, v1 = 0.f, v2 = 0.f, beta = 0.f;
+    const int pl = p - ws;
+    const int nr = (hi - p) >= 3 ? 3 : 2;
+    if (act) {
+      float x0, x1, x2;
+      if (p == lo - 1) {
+        const int l = lo - ws;
+        shift_poly<float>(HW(l, l), HW(l + 1, l), HW(l, l + 1), HW(l + 1, l + 1), (lo + 2 <= hi) ? HW(l + 2, l + 1) : 0.f,
+                          shifts + 4 * j, x0, x1, x2);
+      } else {
+        x0 = HW(pl + 1, pl); x1 = HW(pl + 2, pl); x2 = nr > 2 ? HW(pl + 3, pl) : 0.f;
+      }
+      refl3_fast(nr, x0, x1, x2, beta, tau, v1, v2);
+      __syncwarp();
+    }
+    if (j < nb && lane == 0) {
+      ChaseRec r;
+      r.tau = tau; r.v1 = v1; r.v2 = v2; r.nr = nr;
+      recs_r[(t - t0) * CZ_NB + j] = r;
+    }
+    if (act) {
+      if (tau != 0.f) {
+        if (nr == 3) wl3u<float, ld, NI>(Hw, pl + 1, pl + 1, nw - 1, tau, v1, v2, lane);
+        else wl2u<float, ld, NI>(Hw, pl + 1, pl + 1, nw - 1, tau, v1, lane);
+      }
+      if (p >= lo && lane == 0) {
+        HW(pl + 1, pl) = beta;
+        HW(pl + 2, pl) = 0.f;
+        if (nr > 2) HW(pl + 3, pl) = 0.f;
+      }
+    }
+    named_bar(1, CZ_THREADS);  // bulge warps + the signalling warp
+    if (warp == CZ_NB) {
+      if (lane == 0) {  // every reflector of step t was posted before the barrier
+        __threadfence();
+        *(volatile int*)flag_r = t - t0 + 1;
+      }
+      continue;  // the fence stays off the bulge warps' second barrier
+    }
+    if (act && tau != 0.f) {
+      const int rmax = ((p + 4 < hi) ? p + 4 : hi) - ws;
+      if (nr == 3) wr3h<ld, NI>(Hw, rmax, pl + 1, tau, v1, v2, lane);
+      else wr2h<ld, NI>(Hw, rmax, pl + 1, tau, v1, lane);
+    }
+    named_bar(2, 32 * CZ_NB);
+  }
+  __syncthreads();
+  for (int e = tid; e < nw * nw; e += CZ_THREADS) {
+    const int i = e % nw, jj = e / nw;
+    H[(ws + i) + (size_t)(ws + jj) * ldh] = HW(i, jj);
+  }
+#undef HW
+}
+template <class S>
+constexpr bool kChase2 = std::is_same<S, float>::value && MSY_CHASE2 != 0 && MsCfg<S>::W == CZ_W && MsCfg<S>::NB <= CZ_NB;
 
 // ---------------------------------------------------------------------------
 // in-place application of a small orthogonal Z (nz x nz, ld nz, nz <= ZMAX):
@@ -408,7 +617,14 @@ __global__ void __cluster_dims__(Azc<S>::N, 1, 1) __launch_bounds__(AZC_THREADS)
 // through smem so that global stores are warp-contiguous.
 constexpr int AZF_THREADS = 256, AZF_TILE = 64, AZF_W = 128, AZF_LDZ = 132, AZF_LDT = 65, AZF_LDC = 68;
 constexpr int AZF_TS = 128 * 68;  // floats of the tile / output staging buffer (>= 64 * 132, 128 * 65, 128 * 68)
-static size_t azf_smem() { return (size_t)(AZF_W * AZF_LDZ + AZF_TS) * sizeof(float); }
+#ifndef MSY_FAR_PAD
+#define MSY_FAR_PAD 0  // extra dynamic smem (bytes): > 11 KB leaves one far CTA per SM
+#endif
+static size_t azf_smem() { return (size_t)(AZF_W * AZF_LDZ + AZF_TS) * sizeof(float) + MSY_FAR_PAD; }
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __global__ void __launch_bounds__(AZF_THREADS, 2)
     apply_z_far_kernel(float* H, int ldh, float* U, int ldu, const ApplyJobs<float> jobs) {
   extern __shared__ __align__(16) unsigned char azf_raw[];
@@ -423,20 +639,13 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
   const int cL0 = jobs.cL0[j], cL1 = jobs.cL1[j], rlo = jobs.rlo[j], rR1 = jobs.rR1[j], mU = jobs.mU[j];
   const int ntL = cL1 > cL0 ? cdiv(cL1 - cL0, AZF_TILE) : 0, ntR = rR1 > rlo ? cdiv(rR1 - rlo, AZF_TILE) : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {  // Z, transposed on the way in: thread (k, 4 columns) -> one conflict-free STS.128
-    const int k = tid & 127;
-#pragma unroll 4
-    for (int it = 0; it < 16; it++) {
-      const int o = 4 * ((tid >> 7) + 2 * it);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (k < nz) {
-        if (o < nz) v.x = Zg[k + (size_t)o * nz];
-        if (o + 1 < nz) v.y = Zg[k + (size_t)(o + 1) * nz];
-        if (o + 2 < nz) v.z = Zg[k + (size_t)(o + 2) * nz];
-        if (o + 3 < nz) v.w = Zg[k + (size_t)(o + 3) * nz];
-      }
-      *reinterpret_cast<float4*>(&Zs[k * AZF_LDZ + o]) = v;
-    }
+  // Z, transposed on the way in, and the input tile below: 4-byte cp.async (LDGSTS) per element,
+  // every copy of the CTA in flight at once (a register-staged loop was latency-bound: 25 of the
+  // 31 us a tile took)
+  for (int e = tid; e < AZF_W * AZF_W; e += AZF_THREADS) {
+    const int k = e & 127, o = e >> 7;
+    if (k < nz && o < nz) cp_async4(&Zs[k * AZF_LDZ + o], &Zg[k + (size_t)o * nz]);
+    else Zs[k * AZF_LDZ + o] = 0.f;
   }
   // warp -> (output half h, group of 16 tile columns / rows cq); lane -> (ig, cg)
   const int h = warp & 1, cq = warp >> 1, ig = lane & 7, cg = lane >> 3;
@@ -450,8 +659,10 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
     const int c0 = cL0 + b * AZF_TILE, nc = min(AZF_TILE, cL1 - c0);
     for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {  // lanes along k: coalesced, conflict-free
       const int k = e & 127, c = e >> 7;
-      Ts[k * AZF_LDT + c] = (k < nz && c < nc) ? H[(r0 + k) + (size_t)(c0 + c) * ldh] : 0.f;
+      if (k < nz && c < nc) cp_async4(&Ts[k * AZF_LDT + c], &H[(r0 + k) + (size_t)(c0 + c) * ldh]);
+      else Ts[k * AZF_LDT + c] = 0.f;
     }
+    cp_async_wait_all();
     __syncthreads();
 #pragma unroll 4
     for (int k = 0; k < nz; k++) {
@@ -489,8 +700,10 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
   // ---- regions R / U: M[r, r0 + o] <- sum_k M[r, r0 + k] Z[k, o] ----
   for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {  // lanes along r: coalesced, contiguous smem
     const int r = e & 63, k = e >> 6;
-    Ts[k * AZF_LDC + r] = (k < nz && r < nrows) ? M[(rbase + r) + (size_t)(r0 + k) * ldm] : 0.f;
+    if (k < nz && r < nrows) cp_async4(&Ts[k * AZF_LDC + r], &M[(rbase + r) + (size_t)(r0 + k) * ldm]);
+    else Ts[k * AZF_LDC + r] = 0.f;
   }
+  cp_async_wait_all();
   __syncthreads();
 #pragma unroll 4
   for (int k = 0; k < nz; k++) {

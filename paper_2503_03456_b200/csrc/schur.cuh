@@ -218,6 +218,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
   constexpr int W = MsCfg<S>::W;
   const size_t smem_max = (size_t)(W + 1) * (2 * W) * sizeof(S);  // H window + Z, stride W + 1
   MSY_SMEM_ATTR_ONCE(chase_kernel<S>, smem_max);
+  if constexpr (kChase2<S>) MSY_SMEM_ATTR_ONCE(chase2_kernel, chase2_smem());
   MSY_SMEM_ATTR_ONCE(apply_z_kernel<S>, (int)applyz_smem<S>(W));
   MSY_SMEM_ATTR_ONCE(apply_z_multi_kernel<S>, (int)applyz_smem<S>(W));
   MSY_SMEM_ATTR_ONCE(apply_z_cl_kernel<S>, (int)azc_smem<S>());
@@ -244,7 +245,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
     int we = std::min(ws + W, hi + 1);
     long t1 = t;
     while (t1 < Tn && Uf(t1) <= we - 1) t1++;
-    if (t1 == t || nwins >= 4096) return -5;
+    if (t1 == t || nwins >= 4096 || t1 - t > W + 4 * nb) return -5;  // (a window never holds more steps)
     wins[nwins++] = {ws, we, (int)t, (int)t1};
     t = t1;
   }
@@ -312,7 +313,8 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
       }
       {
         KScope ks(KC_CHASE, 0, st);
-        chase_kernel<S><<<nj, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
+        if constexpr (kChase2<S>) chase2_kernel<<<2 * nj, CZ_THREADS, chase2_smem(), st>>>(H, ldh, lo, hi, nb, cj);
+        else chase_kernel<S><<<nj, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
         MSY_LAUNCH_CK();
       }
       if (ovl && tau > 0) MSY_CK(cudaStreamWaitEvent(st, sc->evD, 0));  // far(tau-1) done
@@ -357,7 +359,8 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
     cj.Z[0] = Zbuf + (k & 1) * ZMAX * ZMAX;
     {
       KScope ks(KC_CHASE, 0, st);
-      chase_kernel<S><<<1, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
+      if constexpr (kChase2<S>) chase2_kernel<<<2, CZ_THREADS, chase2_smem(), st>>>(H, ldh, lo, hi, nb, cj);
+      else chase_kernel<S><<<1, nthr, smem_max, st>>>(H, ldh, lo, hi, nb, cj);
       MSY_LAUNCH_CK();
     }
     if (sc->aux) MSY_CK(cudaEventRecord(sc->evC, st));
