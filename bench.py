@@ -504,7 +504,7 @@ def run_ours(args):
         sch = phases.get("schur")
         if sch and args.variant != "bs":
             traffic, tsrc = ncu_traffic(3)
-            roof = {"bound": "fp32-simt", "kernel": ("Schur phase: hess_panel2 + chase + apply_z_cl + schur_mss "
+            roof = {"bound": "fp32-simt", "kernel": ("Schur phase: hess_panel2 + chase2 + apply_z_far/cl + schur_mss "
                                                      "kernels (the dominant phase of the step)"),
                     "achieved": sch["tflops"], "peak": sch["peak"], "unit": "TFLOP/s", "frac": sch["frac"],
                     "traffic": traffic, "traffic_source": tsrc,
