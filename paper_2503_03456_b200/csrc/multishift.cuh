@@ -36,6 +36,7 @@ template <> struct MsCfg<double> { static constexpr int W = 112, NB = 16; };
 template <> struct MsCfg<cfloat> { static constexpr int W = 112, NB = 16; };
 template <> struct MsCfg<cdouble> { static constexpr int W = 80, NB = 10; };
 constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
+constexpr int ZMASK_OFF = ZMAX * ZMAX - 1;  // chase2_kernel: nonzero-block map of a window factor, in its buffer's last word
 
 // ---------------------------------------------------------------------------
 // window chase: one CTA, one warp per bulge, the W x W window of H and its
@@ -50,6 +51,7 @@ constexpr int ZMAX = 160;  // largest window / block order handled by apply_z
 #define MSY_KMAX 8
 #endif
 constexpr int KMAX = MSY_KMAX;  // bulge chains in flight per sweep (one CTA each)
+constexpr size_t ZT_DELTA = (size_t)2 * KMAX * ZMAX * ZMAX;  // chase2_kernel: row-major copy of a window factor, this far behind it
 // fixed-trip, loads-first warp ops (wl3u / wr3u2) for real fp32 windows; the wider types keep
 // the loop forms (the unrolled register arrays would spill)
 template <class S> constexpr bool kFixedTrip = std::is_same<S, float>::value;
@@ -276,11 +278,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CZ_THREADS)
       }
     }
     __syncthreads();
+    // Z goes out with a 16-bit map of its nonzero 32 x 32 blocks (bit 4 (i / 32) + j / 32): entries
+    // no reflector reached are exact zeros (about half of Z), and the far application skips them
     float* Zg = jobs.Z[job];
+    __shared__ unsigned s_zmask;
+    if (tid == 0) s_zmask = 0u;
+    __syncthreads();
+    unsigned bits = 0u;
     for (int e = tid; e < nw * nw; e += CZ_THREADS) {
       const int i = e % nw, jj = e / nw;
-      Zg[i + (size_t)jj * nw] = Zw[i + jj * CZ_LD];
+      const float z = Zw[i + jj * CZ_LD];
+      Zg[i + (size_t)jj * nw] = z;
+      if (z != 0.f) bits |= 1u << (4 * (i >> 5) + (jj >> 5));
     }
+    float* ZgT = Zg + ZT_DELTA;  // row-major copy: the far application stages it with 16-byte copies
+    for (int e = tid; e < nw * nw; e += CZ_THREADS) {
+      const int o = e % nw, k = e / nw;
+      ZgT[e] = Zw[k + o * CZ_LD];
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (lane == 0 && bits) atomicOr(&s_zmask, bits);
+    __syncthreads();
+    if (tid == 0) reinterpret_cast<unsigned*>(Zg)[ZMASK_OFF] = s_zmask;
     return;
   }
   // ---- rank 0: the chase proper (H window only) ----
@@ -475,6 +494,7 @@ struct ApplyJobs {
   int n;
   int start[KMAX + 1], nz[KMAX], r0[KMAX], cL0[KMAX], cL1[KMAX], rlo[KMAX], rR1[KMAX], mU[KMAX];
   const S* Z[KMAX];
+  int zmask[KMAX];  // 1: Z[j] carries a nonzero-block map at ZMASK_OFF (factors written by chase2_kernel)
 };
 // algorithmic flops of one apply_z_multi launch
 template <class S>
@@ -617,12 +637,21 @@ __global__ void __cluster_dims__(Azc<S>::N, 1, 1) __launch_bounds__(AZC_THREADS)
 // through smem so that global stores are warp-contiguous.
 constexpr int AZF_THREADS = 256, AZF_TILE = 64, AZF_W = 128, AZF_LDZ = 132, AZF_LDT = 65, AZF_LDC = 68;
 constexpr int AZF_TS = 128 * 68;  // floats of the tile / output staging buffer (>= 64 * 132, 128 * 65, 128 * 68)
+#ifndef MSY_FAR_ZT
+#define MSY_FAR_ZT 1     // far application: 16-byte copies (row-major Z copy of chase2, aligned row groups of R / U tiles)
+#endif
+#ifndef MSY_FAR_ZMASK
+#define MSY_FAR_ZMASK 1  // far application skips the zero 32 x 32 blocks of the chase2 window factors
+#endif
 #ifndef MSY_FAR_PAD
 #define MSY_FAR_PAD 0  // extra dynamic smem (bytes): > 11 KB leaves one far CTA per SM
 #endif
 static size_t azf_smem() { return (size_t)(AZF_W * AZF_LDZ + AZF_TS) * sizeof(float) + MSY_FAR_PAD; }
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __global__ void __launch_bounds__(AZF_THREADS, 2)
@@ -642,14 +671,24 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
   // Z, transposed on the way in, and the input tile below: 4-byte cp.async (LDGSTS) per element,
   // every copy of the CTA in flight at once (a register-staged loop was latency-bound: 25 of the
   // 31 us a tile took)
-  for (int e = tid; e < AZF_W * AZF_W; e += AZF_THREADS) {
-    const int k = e & 127, o = e >> 7;
-    if (k < nz && o < nz) cp_async4(&Zs[k * AZF_LDZ + o], &Zg[k + (size_t)o * nz]);
-    else Zs[k * AZF_LDZ + o] = 0.f;
+  if (MSY_FAR_ZT && jobs.zmask[j] && (nz & 3) == 0) {  // chase2 factor: its row-major copy, 16 bytes per copy
+    const float* __restrict__ ZT = Zg + ZT_DELTA;
+    for (int e = tid; e < AZF_W * (AZF_W / 4); e += AZF_THREADS) {
+      const int k = e >> 5, o4 = (e & 31) * 4;
+      if (k < nz && o4 < nz) cp_async16(&Zs[k * AZF_LDZ + o4], &ZT[(size_t)k * nz + o4]);
+      else *reinterpret_cast<float4*>(&Zs[k * AZF_LDZ + o4]) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else {
+    for (int e = tid; e < AZF_W * AZF_W; e += AZF_THREADS) {
+      const int k = e & 127, o = e >> 7;
+      if (k < nz && o < nz) cp_async4(&Zs[k * AZF_LDZ + o], &Zg[k + (size_t)o * nz]);
+      else Zs[k * AZF_LDZ + o] = 0.f;
+    }
   }
   // warp -> (output half h, group of 16 tile columns / rows cq); lane -> (ig, cg)
   const int h = warp & 1, cq = warp >> 1, ig = lane & 7, cg = lane >> 3;
   const int oa = h * 64 + ig * 4, ob = oa + 32, tb = cq * 16 + cg * 4;
+  const unsigned zbits = (MSY_FAR_ZMASK && jobs.zmask[j]) ? reinterpret_cast<const unsigned*>(Zg)[ZMASK_OFF] : 0xffffu;
   float acc[8][4];
 #pragma unroll
   for (int a = 0; a < 8; a++)
@@ -664,18 +703,45 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
     }
     cp_async_wait_all();
     __syncthreads();
+    for (int kb = 0; kb < 4; kb++) {  // 32-deep slices of the contraction; zero blocks of Z skipped
+      const int fa = (zbits >> (4 * kb + 2 * h)) & 1, fb = (zbits >> (4 * kb + 2 * h + 1)) & 1;
+      const int k1 = min(nz, 32 * kb + 32);
+      if (fa && fb) {
 #pragma unroll 4
-    for (int k = 0; k < nz; k++) {
-      const float4 za = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oa]);
-      const float4 zb = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + ob]);
-      const float z[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
-      float t[4];
+        for (int k = 32 * kb; k < k1; k++) {
+          const float4 za = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oa]);
+          const float4 zb = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + ob]);
+          const float z[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+          float t[4];
 #pragma unroll
-      for (int q = 0; q < 4; q++) t[q] = Ts[k * AZF_LDT + tb + q];
+          for (int q = 0; q < 4; q++) t[q] = Ts[k * AZF_LDT + tb + q];
 #pragma unroll
-      for (int a = 0; a < 8; a++)
+          for (int a = 0; a < 8; a++)
 #pragma unroll
-        for (int q = 0; q < 4; q++) acc[a][q] = fmaf(z[a], t[q], acc[a][q]);
+            for (int q = 0; q < 4; q++) acc[a][q] = fmaf(z[a], t[q], acc[a][q]);
+        }
+      } else if (fa || fb) {
+        const int oo = fa ? oa : ob, a0 = fa ? 0 : 4;
+#pragma unroll 4
+        for (int k = 32 * kb; k < k1; k++) {
+          const float4 zv = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oo]);
+          const float z[4] = {zv.x, zv.y, zv.z, zv.w};
+          float t[4];
+#pragma unroll
+          for (int q = 0; q < 4; q++) t[q] = Ts[k * AZF_LDT + tb + q];
+          if (a0 == 0) {
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+              for (int q = 0; q < 4; q++) acc[a][q] = fmaf(z[a], t[q], acc[a][q]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+              for (int q = 0; q < 4; q++) acc[4 + a][q] = fmaf(z[a], t[q], acc[4 + a][q]);
+          }
+        }
+      }
     }
     __syncthreads();
     // outputs staged as Os[c * LDZ + o] (o contiguous, like global memory)
@@ -698,24 +764,67 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
   else { b -= ntR; M = U; ldm = ldu; rbase = b * AZF_TILE; nrows = min(AZF_TILE, mU - rbase); }
   if (nrows <= 0) return;
   // ---- regions R / U: M[r, r0 + o] <- sum_k M[r, r0 + k] Z[k, o] ----
-  for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {  // lanes along r: coalesced, contiguous smem
-    const int r = e & 63, k = e >> 6;
-    if (k < nz && r < nrows) cp_async4(&Ts[k * AZF_LDC + r], &M[(rbase + r) + (size_t)(r0 + k) * ldm]);
-    else Ts[k * AZF_LDC + r] = 0.f;
+  const bool al16 = MSY_FAR_ZT && (ldm & 3) == 0 && (rbase & 3) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0;
+  if (al16) {  // rows in aligned groups of four: 16-byte copies (4-byte ones for a ragged last group)
+    for (int e = tid; e < AZF_W * (AZF_TILE / 4); e += AZF_THREADS) {
+      const int r4 = (e & 15) * 4, k = e >> 4;
+      float* dst = &Ts[k * AZF_LDC + r4];
+      if (k < nz && r4 + 3 < nrows) {
+        cp_async16(dst, &M[(rbase + r4) + (size_t)(r0 + k) * ldm]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          if (k < nz && r4 + q < nrows) cp_async4(dst + q, &M[(rbase + r4 + q) + (size_t)(r0 + k) * ldm]);
+          else dst[q] = 0.f;
+        }
+      }
+    }
+  } else {
+    for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {  // lanes along r: coalesced, contiguous smem
+      const int r = e & 63, k = e >> 6;
+      if (k < nz && r < nrows) cp_async4(&Ts[k * AZF_LDC + r], &M[(rbase + r) + (size_t)(r0 + k) * ldm]);
+      else Ts[k * AZF_LDC + r] = 0.f;
+    }
   }
   cp_async_wait_all();
   __syncthreads();
+  for (int kb = 0; kb < 4; kb++) {
+    const int fa = (zbits >> (4 * kb + 2 * h)) & 1, fb = (zbits >> (4 * kb + 2 * h + 1)) & 1;
+    const int k1 = min(nz, 32 * kb + 32);
+    if (fa && fb) {
 #pragma unroll 4
-  for (int k = 0; k < nz; k++) {
-    const float4 za = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oa]);
-    const float4 zb = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + ob]);
-    const float z[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
-    const float4 tv = *reinterpret_cast<const float4*>(&Ts[k * AZF_LDC + tb]);
-    const float t[4] = {tv.x, tv.y, tv.z, tv.w};
+      for (int k = 32 * kb; k < k1; k++) {
+        const float4 za = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oa]);
+        const float4 zb = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + ob]);
+        const float z[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+        const float4 tv = *reinterpret_cast<const float4*>(&Ts[k * AZF_LDC + tb]);
+        const float t[4] = {tv.x, tv.y, tv.z, tv.w};
 #pragma unroll
-    for (int a = 0; a < 8; a++)
+        for (int a = 0; a < 8; a++)
 #pragma unroll
-      for (int q = 0; q < 4; q++) acc[a][q] = fmaf(t[q], z[a], acc[a][q]);
+          for (int q = 0; q < 4; q++) acc[a][q] = fmaf(t[q], z[a], acc[a][q]);
+      }
+    } else if (fa || fb) {
+      const int oo = fa ? oa : ob, a0 = fa ? 0 : 4;
+#pragma unroll 4
+      for (int k = 32 * kb; k < k1; k++) {
+        const float4 zv = *reinterpret_cast<const float4*>(&Zs[k * AZF_LDZ + oo]);
+        const float z[4] = {zv.x, zv.y, zv.z, zv.w};
+        const float4 tv = *reinterpret_cast<const float4*>(&Ts[k * AZF_LDC + tb]);
+        const float t[4] = {tv.x, tv.y, tv.z, tv.w};
+        if (a0 == 0) {
+#pragma unroll
+          for (int a = 0; a < 4; a++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[a][q] = fmaf(t[q], z[a], acc[a][q]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < 4; a++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[4 + a][q] = fmaf(t[q], z[a], acc[4 + a][q]);
+        }
+      }
+    }
   }
   __syncthreads();
   // outputs staged as Os[o * LDC + r] (r contiguous, like global memory)
@@ -725,9 +834,25 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
     *reinterpret_cast<float4*>(&Ts[o * AZF_LDC + tb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
   }
   __syncthreads();
-  for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {
-    const int r = e & 63, o = e >> 6;
-    if (o < nz && r < nrows) M[(rbase + r) + (size_t)(r0 + o) * ldm] = Ts[o * AZF_LDC + r];
+  if (al16) {
+    for (int e = tid; e < AZF_W * (AZF_TILE / 4); e += AZF_THREADS) {
+      const int r4 = (e & 15) * 4, o = e >> 4;
+      if (o >= nz) continue;
+      float* dst = &M[(rbase + r4) + (size_t)(r0 + o) * ldm];
+      const float4 v = *reinterpret_cast<const float4*>(&Ts[o * AZF_LDC + r4]);
+      if (r4 + 3 < nrows) {
+        *reinterpret_cast<float4*>(dst) = v;
+      } else {
+        if (r4 < nrows) dst[0] = v.x;
+        if (r4 + 1 < nrows) dst[1] = v.y;
+        if (r4 + 2 < nrows) dst[2] = v.z;
+      }
+    }
+  } else {
+    for (int e = tid; e < AZF_W * AZF_TILE; e += AZF_THREADS) {
+      const int r = e & 63, o = e >> 6;
+      if (o < nz && r < nrows) M[(rbase + r) + (size_t)(r0 + o) * ldm] = Ts[o * AZF_LDC + r];
+    }
   }
 }
 // launch for a job list whose `start` was built for 32-wide tiles: rebuilt here for 64-wide ones

@@ -48,7 +48,7 @@ struct SchurLoopWs {
   S* Zend;    // Schur vectors of the endgame blocks (sum of block orders^2 <= NMAX * m)
   int* dend;  // their [status, sweeps] words
   static void carve(Arena& ar, int m, SchurLoopWs& w) {
-    w.Z = ar.get<S>((size_t)2 * KMAX * ZMAX * ZMAX);
+    w.Z = ar.get<S>((size_t)4 * KMAX * ZMAX * ZMAX);  // second half: row-major copies (ZT_DELTA)
     w.sblk = ar.get<S>((size_t)EigCfg<S>::NMAX * EigCfg<S>::NMAX);
     w.wr = ar.get<R>(256);
     w.wi = ar.get<R>(256);
@@ -289,6 +289,7 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
         const int rn = std::max(0, std::min(w.ws - W, rstar));
         for (int f = 0; f < 2; f++) {
           ApplyJobs<S>& r = jr[f];
+          r.zmask[nj] = jc[f].zmask[nj] = kChase2<S> ? 1 : 0;
           r.nz[nj] = nz; r.Z[nj] = Zc; r.r0[nj] = w.ws; r.rR1[nj] = 0; r.mU[nj] = 0;
           r.cL0[nj] = f == 0 ? w.we : cn;
           r.cL1[nj] = f == 0 ? cn : m;
