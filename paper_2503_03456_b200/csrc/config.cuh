@@ -55,7 +55,7 @@
 #define MSY_NO_STREAM_PRIORITY 0
 #endif
 #ifndef MSY_LANE_HESS_CAP
-#define MSY_LANE_HESS_CAP 0    // cap on each batched lane's cooperative Hessenberg grid (0: none)
+#define MSY_LANE_HESS_CAP 8    // cap on each batched lane's cooperative Hessenberg grid (0: none; m = 512: 16 -> 184, 8 -> 245, 4 -> 238 solves/s)
 #endif
 #ifndef MSY_FAR_MIN_TILES
 #define MSY_FAR_MIN_TILES 64   // single-job Z applications of at least this many 32-wide tiles use the far kernel (-1: far kernel off)

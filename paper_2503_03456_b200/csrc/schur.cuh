@@ -29,6 +29,9 @@ namespace msy {
 #ifndef MSY_SUBMAX
 #define MSY_SUBMAX 640  // detached blocks up to this order are factored beside the sweeps (0: off)
 #endif
+#ifndef MSY_SUB_PRIO
+#define MSY_SUB_PRIO 1  // helper streams: 0 least, 1 middle, 2 greatest priority
+#endif
 #ifndef MSY_SUB_HELPERS
 #define MSY_SUB_HELPERS 3
 #endif
@@ -125,7 +128,7 @@ struct SubHelper {
     int lo_pri = 0, hi_pri = 0;
     cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
     for (int i = 0; i < NH; i++) {
-      cudaStreamCreateWithPriority(&st[i], cudaStreamNonBlocking, (lo_pri + hi_pri) / 2);
+      cudaStreamCreateWithPriority(&st[i], cudaStreamNonBlocking, MSY_SUB_PRIO == 2 ? hi_pri : (MSY_SUB_PRIO == 0 ? lo_pri : (lo_pri + hi_pri) / 2));
       cudaEventCreateWithFlags(&ev1[i], cudaEventDisableTiming);
       std::thread([this, dev, i]() {
         cudaSetDevice(dev);
@@ -300,6 +303,10 @@ int ms_sweep(int m, S* H, int ldh, S* U, int ldu, int lo, int hi, int nb, int K,
         jc[1].nz[nj] = nz; jc[1].Z[nj] = Zc; jc[1].r0[nj] = w.ws; jc[1].cL0[nj] = jc[1].cL1[nj] = 0;
         jc[1].rR1[nj] = rn; jc[1].mU[nj] = m;
         jc[0].rlo[nj] = rn;
+        if (!ovl) {  // one stream (batched lanes): whole row regions, then whole column regions + U
+          jr[0].cL1[nj] = m; jr[1].cL0[nj] = jr[1].cL1[nj] = 0;
+          jc[0].rlo[nj] = 0; jc[0].mU[nj] = m; jc[1].rR1[nj] = 0; jc[1].mU[nj] = 0;
+        }
         nj++;
       }
       if (nj == 0) continue;
@@ -610,13 +617,12 @@ int schur_qr_loop(int m, S* A, int lda, S* U, int ldu, SchurLoopWs<S>& w, cudaSt
       K = std::max(1, std::min({std::min(kmax_env, KMAX), EigCfg<S>::NMAX / (2 * nb), sz / (12 * nb)}));
     ns = 2 * nb * K;
     if (!exc) {
-      const S* src = A + (hi - ns + 1) + (size_t)(hi - ns + 1) * lda;
-      copy_block_kernel<S><<<dim3(cdiv(ns, 128), ns), 128, 0, st>>>(ns, src, lda, w.sblk, ns);
-      MSY_LAUNCH_CK();
+      // the eigenvalue-only kernel stages the trailing block from A itself and writes nothing back
+      S* src = A + (hi - ns + 1) + (size_t)(hi - ns + 1) * lda;
       // shifts need not be converged to working accuracy: a looser deflation tolerance
       // cuts the eigenvalue iteration roughly in half
       constexpr double stol = MSY_SHIFT_TOL;
-      rc = schur_small_launch<S>(ns, w.sblk, ns, nullptr, 0, SS_EIGONLY, w.wr, w.wi, w.dinfo + 16, st,
+      rc = schur_small_launch<S>(ns, src, lda, nullptr, 0, SS_EIGONLY, w.wr, w.wi, w.dinfo + 16, st,
                                  (R)std::max<double>(stol, tr<S>::u()));
       if (rc) return rc;
     }

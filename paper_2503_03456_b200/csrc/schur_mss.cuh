@@ -629,11 +629,12 @@ __global__ void __launch_bounds__(32 * MSY_MSS_NWARP) schur_mss_kernel(int n, S*
   }
   if (tid == 0) { sh.status = status; }
   __syncthreads();
-  for (int e = tid; e < n * n; e += nt) {
-    int r = e % n, c = e / n;
-    Hg[r + (size_t)c * ldh] = HH(r, c);
-    if (wantz) Zg[r + (size_t)c * ldz] = ZZ(r, c);
-  }
+  if (!eigonly)  // eigenvalue-only calls (the sweeps' shifts) read the matrix in place and leave it alone
+    for (int e = tid; e < n * n; e += nt) {
+      int r = e % n, c = e / n;
+      Hg[r + (size_t)c * ldh] = HH(r, c);
+      if (wantz) Zg[r + (size_t)c * ldz] = ZZ(r, c);
+    }
   if (tid == 0 && info) {
     info[0] = sh.status;
     info[1] = total;

@@ -957,6 +957,7 @@ int sylv_solve_batched(const sylv_params* p, int batch, const void* const* A, in
     // many lanes' cooperative Hessenberg panels must be co-resident: small grids per lane
     const int cap_saved = hess_grid_cap();
     hess_grid_cap() = MSY_LANE_HESS_CAP;
+    hess_graph_lane() = true;
     cudaStreamWaitEvent(ls.st, start, 0);
     char* mine = (char*)ws + one * (size_t)lane;
     for (int i; (i = next.fetch_add(1)) < batch && err.load() == 0;) {
@@ -968,6 +969,7 @@ int sylv_solve_batched(const sylv_params* p, int batch, const void* const* A, in
     host_sync_blocking() = false;
     t_serial_lane = false;
     hess_grid_cap() = cap_saved;
+    hess_graph_lane() = false;
   };
   LanePool::get().run(nl, fn);
   for (int l = 0; l < nl; l++)

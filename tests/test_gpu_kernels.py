@@ -314,3 +314,20 @@ def test_solve_hermitian_matches_kronecker(B200, rng, m, n, cplx):
     with pytest.raises(B200.SingularEquationError):
         B200.solve_hermitian(B200.SylvesterProblem(np.diag([1.0, 2.0]), np.diag([-2.0]), np.ones((2, 1)),
                                                    kind="hermitian"))
+
+
+@pytest.mark.gpu
+def test_schur_run_to_run_identical():
+    """The large Schur runs detached blocks on helper threads and far applications on side
+    streams; every entry still receives its operations in one fixed order, so two runs of the
+    same matrix agree bit for bit (a race between the streams would show up here)."""
+    import torch
+    from paper_2503_03456_b200.linalg import schur_tensor
+    torch.manual_seed(5)
+    m = 1500
+    A = (torch.randn(m, m, device="cuda", dtype=torch.float64) / m ** 0.5 + 2 * torch.eye(m, device="cuda",
+                                                                                       dtype=torch.float64)).float()
+    T1, U1 = schur_tensor(A.clone(), [])
+    T2, U2 = schur_tensor(A.clone(), [])
+    torch.cuda.synchronize()
+    assert torch.equal(T1, T2) and torch.equal(U1, U2)
