@@ -637,6 +637,9 @@ __global__ void __cluster_dims__(Azc<S>::N, 1, 1) __launch_bounds__(AZC_THREADS)
 // through smem so that global stores are warp-contiguous.
 constexpr int AZF_THREADS = 256, AZF_TILE = 64, AZF_W = 128, AZF_LDZ = 132, AZF_LDT = 65, AZF_LDC = 68;
 constexpr int AZF_TS = 128 * 68;  // floats of the tile / output staging buffer (>= 64 * 132, 128 * 65, 128 * 68)
+#ifndef MSY_FAR_BULK
+#define MSY_FAR_BULK 1   // far application: cp.async.bulk + mbarrier for full tiles
+#endif
 #ifndef MSY_FAR_ZT
 #define MSY_FAR_ZT 1     // far application: 16-byte copies (row-major Z copy of chase2, aligned row groups of R / U tiles)
 #endif
@@ -653,6 +656,42 @@ __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)), "l"(gsrc) : "memory");
 }
+// ---- bulk asynchronous copies (the TMA engine's linear form, cp.async.bulk) with an mbarrier ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(mbar)), "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes, unsigned long long* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __global__ void __launch_bounds__(AZF_THREADS, 2)
     apply_z_far_kernel(float* H, int ldh, float* U, int ldu, const ApplyJobs<float> jobs) {
@@ -671,7 +710,29 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
   // Z, transposed on the way in, and the input tile below: 4-byte cp.async (LDGSTS) per element,
   // every copy of the CTA in flight at once (a register-staged loop was latency-bound: 25 of the
   // 31 us a tile took)
-  if (MSY_FAR_ZT && jobs.zmask[j] && (nz & 3) == 0) {  // chase2 factor: its row-major copy, 16 bytes per copy
+  // Full tiles of chase2 factors move with bulk asynchronous copies (cp.async.bulk, the TMA engine):
+  // one 512-byte row of the row-major Z copy and one 256-byte column of an R / U tile per thread,
+  // completion on an mbarrier; ragged tiles and region L keep the cp.async paths below.
+  __shared__ __align__(8) unsigned long long mbar;
+  const bool bulkz = MSY_FAR_BULK && MSY_FAR_ZT && jobs.zmask[j] && nz == AZF_W;
+  bool bulkt = false;
+  {
+    int bb = b - ntL;
+    if (bulkz && bb >= 0) {
+      const float* Mb; int ldb, rb, nr;
+      if (bb < ntR) { Mb = H; ldb = ldh; rb = rlo + bb * AZF_TILE; nr = min(AZF_TILE, rR1 - rb); }
+      else { bb -= ntR; Mb = U; ldb = ldu; rb = bb * AZF_TILE; nr = min(AZF_TILE, mU - rb); }
+      bulkt = nr == AZF_TILE && (ldb & 3) == 0 && (rb & 3) == 0 && (reinterpret_cast<uintptr_t>(Mb) & 15) == 0;
+    }
+  }
+  if (bulkz) {
+    if (tid == 0) {
+      mbar_init(&mbar, 1);
+      mbar_expect_tx(&mbar, (unsigned)(AZF_W * AZF_W * sizeof(float)) + (bulkt ? (unsigned)(AZF_W * AZF_TILE * sizeof(float)) : 0u));
+    }
+    __syncthreads();
+    if (tid < AZF_W) bulk_g2s(&Zs[tid * AZF_LDZ], Zg + ZT_DELTA + (size_t)tid * AZF_W, AZF_W * sizeof(float), &mbar);
+  } else if (MSY_FAR_ZT && jobs.zmask[j] && (nz & 3) == 0) {  // chase2 factor: its row-major copy, 16 bytes per copy
     const float* __restrict__ ZT = Zg + ZT_DELTA;
     for (int e = tid; e < AZF_W * (AZF_W / 4); e += AZF_THREADS) {
       const int k = e >> 5, o4 = (e & 31) * 4;
@@ -702,6 +763,7 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
       else Ts[k * AZF_LDT + c] = 0.f;
     }
     cp_async_wait_all();
+    if (bulkz) mbar_wait(&mbar, 0);
     __syncthreads();
     for (int kb = 0; kb < 4; kb++) {  // 32-deep slices of the contraction; zero blocks of Z skipped
       const int fa = (zbits >> (4 * kb + 2 * h)) & 1, fb = (zbits >> (4 * kb + 2 * h + 1)) & 1;
@@ -762,10 +824,16 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
   int ldm, rbase, nrows;
   if (b < ntR) { M = H; ldm = ldh; rbase = rlo + b * AZF_TILE; nrows = min(AZF_TILE, rR1 - rbase); }
   else { b -= ntR; M = U; ldm = ldu; rbase = b * AZF_TILE; nrows = min(AZF_TILE, mU - rbase); }
-  if (nrows <= 0) return;
+  if (nrows <= 0) {  // (cannot happen for a tile index inside the job; never leave copies in flight)
+    cp_async_wait_all();
+    if (bulkz) mbar_wait(&mbar, 0);
+    return;
+  }
   // ---- regions R / U: M[r, r0 + o] <- sum_k M[r, r0 + k] Z[k, o] ----
   const bool al16 = MSY_FAR_ZT && (ldm & 3) == 0 && (rbase & 3) == 0 && (reinterpret_cast<uintptr_t>(M) & 15) == 0;
-  if (al16) {  // rows in aligned groups of four: 16-byte copies (4-byte ones for a ragged last group)
+  if (bulkt) {  // column k of the tile: 64 contiguous rows, one bulk copy
+    if (tid < AZF_W) bulk_g2s(&Ts[tid * AZF_LDC], &M[rbase + (size_t)(r0 + tid) * ldm], AZF_TILE * sizeof(float), &mbar);
+  } else if (al16) {  // rows in aligned groups of four: 16-byte copies (4-byte ones for a ragged last group)
     for (int e = tid; e < AZF_W * (AZF_TILE / 4); e += AZF_THREADS) {
       const int r4 = (e & 15) * 4, k = e >> 4;
       float* dst = &Ts[k * AZF_LDC + r4];
@@ -787,6 +855,7 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
     }
   }
   cp_async_wait_all();
+  if (bulkz) mbar_wait(&mbar, 0);
   __syncthreads();
   for (int kb = 0; kb < 4; kb++) {
     const int fa = (zbits >> (4 * kb + 2 * h)) & 1, fb = (zbits >> (4 * kb + 2 * h + 1)) & 1;
@@ -833,8 +902,12 @@ __global__ void __launch_bounds__(AZF_THREADS, 2)
     const int o = a < 4 ? oa + a : ob + (a - 4);
     *reinterpret_cast<float4*>(&Ts[o * AZF_LDC + tb]) = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
   }
+  if (bulkt) fence_proxy_async();  // the staged outputs become visible to the bulk-copy engine
   __syncthreads();
-  if (al16) {
+  if (bulkt) {  // column o of the output: one bulk store from the staging buffer
+    if (tid < AZF_W) bulk_s2g(&M[rbase + (size_t)(r0 + tid) * ldm], &Ts[tid * AZF_LDC], AZF_TILE * sizeof(float));
+    bulk_commit_wait_read();
+  } else if (al16) {
     for (int e = tid; e < AZF_W * (AZF_TILE / 4); e += AZF_THREADS) {
       const int r4 = (e & 15) * 4, o = e >> 4;
       if (o >= nz) continue;
