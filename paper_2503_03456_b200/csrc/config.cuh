@@ -27,18 +27,6 @@
 #ifndef MSY_NB_CHAIN
 #define MSY_NB_CHAIN 0         // bulges per chain (0: MsCfg<S>::NB)
 #endif
-#ifndef MSY_AED
-#define MSY_AED 0              // aggressive early deflation in the large Schur loop (measured slower, section 9)
-#endif
-#ifndef MSY_AED_NW
-#define MSY_AED_NW 128
-#endif
-#ifndef MSY_AED_GMAX
-#define MSY_AED_GMAX 16
-#endif
-#ifndef MSY_AED_NIBBLE
-#define MSY_AED_NIBBLE 14
-#endif
 #ifndef MSY_SHIFT_TOL
 #define MSY_SHIFT_TOL 1e-3     // deflation tolerance of the eigenvalue-only shift computation
 #endif

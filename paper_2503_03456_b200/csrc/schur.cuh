@@ -12,7 +12,6 @@
 #include "multishift.cuh"
 #include "schur_small.cuh"
 #include "schur_mss.cuh"
-#include "aed.cuh"
 #include "util.cuh"
 
 #include <chrono>
@@ -47,7 +46,6 @@ struct SchurLoopWs {
   R* wi;
   R* shifts;  // 4 per bulge
   int* dinfo; // small device ints
-  S* vaed;    // AED window Schur vectors
   S* Zend;    // Schur vectors of the endgame blocks (sum of block orders^2 <= NMAX * m)
   int* dend;  // their [status, sweeps] words
   static void carve(Arena& ar, int m, SchurLoopWs& w) {
@@ -57,7 +55,6 @@ struct SchurLoopWs {
     w.wi = ar.get<R>(256);
     w.shifts = ar.get<R>(4 * 128);
     w.dinfo = ar.get<int>(64);
-    w.vaed = m > SmallCfg<S>::NMAX ? ar.get<S>((size_t)AedCfg<S>::NW * AedCfg<S>::NW) : nullptr;
     w.Zend = m > SmallCfg<S>::NMAX ? ar.get<S>((size_t)SmallCfg<S>::NMAX * (m + SmallCfg<S>::NMAX)) : nullptr;
     w.dend = m > SmallCfg<S>::NMAX ? ar.get<int>(2 * (size_t)(m + 1)) : nullptr;
   }
@@ -555,61 +552,7 @@ int schur_qr_loop(int m, S* A, int lda, S* U, int ldu, SchurLoopWs<S>& w, cudaSt
     // bulges per chain (a chain of nb bulges spans 4 nb rows of the W-row chase window)
     const int NBc = std::max(2, std::min(MsCfg<S>::NB, MSY_NB_CHAIN > 0 ? MSY_NB_CHAIN : MsCfg<S>::NB));
     bool exc = (stag > 0 && stag % 6 == 0);
-    // ---- aggressive early deflation on the trailing window (aed.cuh) ----
-    constexpr int aed_on = MSY_AED;
-    constexpr int aed_nw = MSY_AED_NW;
-    constexpr int aed_gmax = MSY_AED_GMAX;
-    constexpr int aed_nibble = MSY_AED_NIBBLE;
-    int aed_ls = 0;
-    if (aed_on && !exc) {
-      const int nw = std::max(16, std::min({aed_nw, AedCfg<S>::NW, sz - 1}));
-      const int kwtop = hi - nw + 1;
-      const S* src = A + kwtop + (size_t)kwtop * lda;
-      copy_block_kernel<S><<<dim3(cdiv(nw, 128), nw), 128, 0, st>>>(nw, src, lda, w.sblk, nw);
-      MSY_LAUNCH_CK();
-      rc = schur_small_launch<S>(nw, w.sblk, nw, w.vaed, nw, SS_WANTZ, nullptr, nullptr, w.dinfo + 32, st);
-      if (rc) return rc;
-      MSY_SMEM_ATTR_ONCE(aed_kernel<S>, (int)aed_smem_bytes<S>());
-      KScope ks(KC_AED, 0, st);
-      aed_kernel<S><<<1, AED_THREADS, aed_smem_bytes<S>(), st>>>(nw, w.sblk, w.vaed, A, lda, kwtop, lo, w.wr, w.wi,
-                                                                 w.dinfo + 40, aed_gmax, w.dinfo + 32);
-      MSY_LAUNCH_CK();
-      int ainfo[12];
-      MSY_CK(d2h(ainfo, w.dinfo + 32, 12 * sizeof(int), st));
-      const int nd = ainfo[8];
-      aed_ls = ainfo[9];
-      loc.aed_calls++;
-      loc.aed_deflated += nd;
-      if (nd > 0) {
-        rc = apply_z<S>(m, nw, w.vaed, A, lda, U, ldu, kwtop, st);
-        if (rc) return rc;
-      }
-      pt.lap(&loc.ms_aed);
-      if (nd > 0 && 100 * nd > aed_nibble * nw) continue;  // enough deflated: re-examine before sweeping
-      if (nd > 0) {
-        hi -= nd;
-        last_hi = hi;
-        stag = 0;
-        sz = hi - lo + 1;
-        if (sz <= NMIN) continue;
-      }
-    }
     int nb, K = 1, ns;
-    if (aed_ls >= 8) {  // shifts: the undeflated window eigenvalues, bottom-most first
-      const int npairs = aed_ls / 2 - 1;
-      nb = std::min({NBc, npairs, std::max(1, (sz - 8) / 8)});
-      if (nb == NBc && kmax_env > 1)
-        K = std::max(1, std::min({std::min(kmax_env, KMAX), npairs / nb, sz / (12 * nb)}));
-      pair_shifts_kernel<S><<<1, 32, 0, st>>>(aed_ls, w.wr, w.wi, nb * K, w.shifts, 0, A, lda, lo, hi, w.dinfo + 24);
-      MSY_LAUNCH_CK();
-      pt.lap(&loc.ms_shift);
-      rc = ms_sweep<S>(m, A, lda, U, ldu, lo, hi, nb, K, w.shifts, w.Z, st, &loc.windows, sc);
-      if (rc) return rc;
-      pt.lap(&loc.ms_sweep);
-      loc.sweeps++;
-      loc.ms_sweeps++;
-      continue;
-    }
     nb = std::min(NBc, std::max(1, (sz - 8) / 8));
     // several chains per sweep when the active block is large and the trailing
     // block that supplies their shifts fits the one-CTA kernel
