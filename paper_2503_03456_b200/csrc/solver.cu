@@ -351,15 +351,21 @@ int run_schur_pair(int m, int n, int kind, const Hh* A, int lda, const Hh* B, in
   const bool blocking = host_sync_blocking();
   int nsm = 0;
   MSY_CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  struct CapGuard {  // half the SMs per Hessenberg panel grid while the pair runs
+  // the two cooperative Hessenberg panel grids share the SMs in proportion to the matrices'
+  // sizes (m = n: half each; C2's 4096 / 2048 pair: 118 / 30, so the large reduction is not
+  // held to half the GPU long after the small one is done)
+  const double wa = (double)m * m, wb = (double)n * n;
+  const int cap_sm_a = std::max(16, std::min(nsm - 16, (int)(nsm * (wa / (wa + wb)) + 0.5)));
+  const int cap_sm_b = nsm - cap_sm_a;
+  struct CapGuard {
     int old;
     explicit CapGuard(int c) : old(hess_grid_cap()) { hess_grid_cap() = c; }
     ~CapGuard() { hess_grid_cap() = old; }
-  } cap_a(nsm / 2);
+  } cap_a(cap_sm_a);
   std::function<void()> job_b = [&]() {
     cudaSetDevice(dev);
     host_sync_blocking() = blocking;
-    hess_grid_cap() = nsm / 2;
+    hess_grid_cap() = cap_sm_b;
     rcb = convert<Ll, Hh>(n, n, B, ldb, w.TB, n, ovf_b, side);
     if (!rcb) rcb = schur_device<Ll>(n, w.TB, n, w.UB, n, w.swB, side, sb, scb);
     if (!rcb && post_b && sb->status == 0) rcb = (*post_b)(side);
